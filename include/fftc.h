@@ -1,0 +1,131 @@
+/*
+ * fftc.h -- C ABI of libfftc.so: batched 1D complex DFT on NVIDIA B200 (sm_100a).
+ *
+ * The operation (§Background): for each of `batch` independent
+ * transforms,
+ *     Y[b, k] = sum_{n=0}^{N-1} X[b, n] * w^{n k},   w = exp(sign * 2*pi*i / N),
+ * unnormalised, natural order, out of place.  sign = -1 is the paper's DFT_N
+ * (w_N = exp(-2*pi*i/N)); sign = +1 is the unnormalised inverse (our reading,
+ * DESIGN.md §3 #1).  It is computed as the paper's general-radix
+ * decimation-in-time Cooley-Tukey factorization (Eq. 2)
+ *     DFT_N = (DFT_K (x) I_M) D^N_M (I_K (x) DFT_M) Pi^N_K,   N = M K,
+ * applied recursively: each Stockham stage of the fused kernels is one level of
+ * Eq. 2, the four-step path is Eq. 2 once at the top with M, K both large, and
+ * the distributed six-step path realises Pi^N_K as NCCL all-to-alls.
+ *
+ * Data layout: `in` / `out` hold batch*N complex64 values, interleaved
+ * (re, im) fp32; element (b, n) is at float offset 2*(b*N + n).
+ * Device pointers unless the function says HOST.  All pointers must be
+ * 16-byte aligned.  The caller owns in/out; `in` is never written.
+ *
+ * Errors: every call returns a status (never aborts).  A kernel fault is
+ * reported by the next call that checks, as in CUDA.
+ *
+ * Thread safety: plans are immutable after create.  Single-pass plans are
+ * re-entrant across streams.  Plans with a workspace (four-step, six-step,
+ * host-staged execution) must not be executed concurrently on two streams.
+ */
+#ifndef FFTC_H_
+#define FFTC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct fftc_plan fftc_plan; /* opaque */
+
+typedef enum {
+  FFTC_SUCCESS = 0,
+  FFTC_ERROR_INVALID_VALUE = 1,    /* N < 1, batch < 0, sign not in {-1,+1}, NULL pointer,
+                                      in == out or overlapping buffers */
+  FFTC_ERROR_UNSUPPORTED_SIZE = 2, /* N has a prime factor > 7 (and is > 1); N*batch*8 overflows;
+                                      dist: nranks does not divide M and K */
+  FFTC_ERROR_MISALIGNED = 3,       /* in / out not 16-byte aligned */
+  FFTC_ERROR_OUT_OF_MEMORY = 4,    /* twiddle table / workspace allocation failed */
+  FFTC_ERROR_CUDA = 5,             /* CUDA launch / runtime error (cudaGetLastError captured) */
+  FFTC_ERROR_NCCL = 6,             /* distributed plan: NCCL failure */
+  FFTC_ERROR_NO_DEVICE = 7         /* no CUDA device / not an sm_100 device */
+} fftc_status;
+
+/* Create a plan for `batch` transforms of length N with direction `sign`.
+ * Factors N into the radix schedule (planner, "N = MK" applied
+ * recursively), builds fp32 twiddle tables from double on the host and
+ * uploads them to the current device; allocates the four-step workspace
+ * (N*batch*8 bytes) when N exceeds the single-pass limit (4096).
+ * batch == 0 is valid (execute is then a no-op).  N == 1 is a copy.
+ * Returns NULL on failure; the reason is fftc_last_error().               */
+fftc_plan* fftc_plan_create(int64_t N, int64_t batch, int sign);
+
+/* Enqueue the transform on `stream` (a cudaStream_t; NULL = legacy default
+ * stream).  Asynchronous: never synchronises the host.  in/out: device
+ * pointers as described above, out-of-place (in != out, no overlap).      */
+fftc_status fftc_execute(const fftc_plan* plan, const void* in, void* out, void* stream);
+
+/* End-to-end form of fftc_execute on HOST buffers (pinned or pageable):
+ * copies in -> device, runs the transform, copies the result back, in
+ * chunks of transforms pipelined over two streams so host<->device copies
+ * overlap the kernels.  Synchronous: returns after `out` is written.
+ * Uses a plan-owned device staging area (allocated on first use).         */
+fftc_status fftc_execute_host(fftc_plan* plan, const void* host_in, void* host_out);
+
+/* Free tables and workspace.  NULL-safe. */
+void fftc_plan_destroy(fftc_plan* plan);
+
+/* Status of the last fftc_plan_create on this thread. */
+fftc_status fftc_last_error(void);
+const char* fftc_status_string(fftc_status s);
+
+/* Human-readable plan summary into buf (radices, passes, kernel, workspace
+ * bytes, launches per execute).  Returns the number of characters written
+ * (excluding NUL), or -1 if plan is NULL.                                  */
+int fftc_plan_describe(const fftc_plan* plan, char* buf, size_t len);
+
+/* Number of kernel launches one fftc_execute of this plan enqueues. */
+int fftc_plan_launches(const fftc_plan* plan);
+
+/* Planner, host only (no device needed): the radix schedule R_0..R_{S-1}
+ * (R_0 = innermost, leaf DFT; prod R_s = N) the single-pass path uses for N.
+ * Writes up to `max` radices, returns the stage count S (0 for N == 1), or
+ * -1 if N < 1 or N has a prime factor > 7.  For N above the single-pass
+ * limit this is the schedule of the whole length; the executed path is
+ * given by fftc_plan_split().                                              */
+int fftc_factorize(int64_t N, int* radices, int max);
+
+/* Top-level split used for N: returns 1 (single pass: *M = N, *K = 1),
+ * 2 (four-step: N = M*K, column DFT_M then row DFT_K), or -1 unsupported. */
+int fftc_plan_split(int64_t N, int64_t* M, int64_t* K);
+
+/* ---------------------------------------------------------------------
+ * Distributed six-step (one process per GPU, NCCL over NVLink/NVSwitch).
+ * A single transform of length N is block-distributed: rank p holds
+ * elements [p*N/P, (p+1)*N/P) of the input and of the output, both in
+ * natural order.  N = M*K with P | M and P | K; the three all-to-alls
+ * realise the global stride permutations of Eq. 2 (Pi^N_K).
+ * ------------------------------------------------------------------- */
+
+/* Size of the opaque NCCL unique id blob. */
+#define FFTC_NCCL_ID_BYTES 128
+
+/* Rank 0 calls this and broadcasts the 128 bytes to the other ranks
+ * (e.g. over torch.distributed).  Returns FFTC_SUCCESS or FFTC_ERROR_NCCL. */
+fftc_status fftc_dist_get_unique_id(void* id_out);
+
+/* Collective over `nranks` processes; each calls it with the same N, sign
+ * and id and its own rank, with its GPU current.  nranks == 1 is allowed
+ * (no communicator; local transposes).  Returns NULL on failure.
+ * `loopback` != 0 runs all nranks virtual ranks inside this one process on
+ * the current GPU (the all-to-alls become device copies; id/rank ignored):
+ * in/out then hold the whole N-element vector.                            */
+fftc_plan* fftc_dist_plan_create(int64_t N, int sign, const void* nccl_id, int rank, int nranks,
+                                 int loopback);
+
+/* fftc_execute on a distributed plan: in / out are this rank's
+ * N/nranks-element natural-order slabs (device). */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FFTC_H_ */

@@ -1,0 +1,206 @@
+"""paper_2207_06803_b200 -- batched 1D complex DFT on B200 (sm_100a), Python binding.
+
+Thin ctypes binding over ``libfftc.so`` (C ABI declared in ``include/fftc.h``).
+Argument marshalling only: every step of the transform runs in the library's
+CUDA kernels.  torch supplies device memory and streams.  There is no CPU
+fallback: if the library or a CUDA device is missing, calls raise.
+
+Functions keep the C names (``fftc_plan_create``, ``fftc_execute``,
+``fftc_execute_host``, ``fftc_plan_destroy``, ``fftc_last_error``,
+``fftc_status_string``, ``fftc_plan_describe``, ``fftc_plan_launches``,
+``fftc_factorize``, ``fftc_plan_split``, ``fftc_dist_get_unique_id``,
+``fftc_dist_plan_create``); :class:`Plan` is a convenience wrapper that owns a
+plan handle and takes contiguous ``torch.complex64`` CUDA tensors.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libfftc.so")
+
+FFTC_SUCCESS = 0
+FFTC_ERROR_INVALID_VALUE = 1
+FFTC_ERROR_UNSUPPORTED_SIZE = 2
+FFTC_ERROR_MISALIGNED = 3
+FFTC_ERROR_OUT_OF_MEMORY = 4
+FFTC_ERROR_CUDA = 5
+FFTC_ERROR_NCCL = 6
+FFTC_ERROR_NO_DEVICE = 7
+FFTC_NCCL_ID_BYTES = 128
+
+_lib = None
+
+
+class FFTCError(RuntimeError):
+    def __init__(self, status: int, what: str = ""):
+        self.status = status
+        super().__init__("%s: %s" % (what or "fftc", fftc_status_string(status)))
+
+
+def load(path: str = LIB_PATH):
+    """Load libfftc.so (raises if it has not been built -- no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError("libfftc.so not built: run `python -m paper_2207_06803_b200.build` "
+                          "(or __graft_entry__.build()); there is no CPU fallback")
+    lib = ctypes.CDLL(path)
+    vp, i64, i32, sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_size_t
+    sig = {
+        "fftc_plan_create": ([i64, i64, i32], vp),
+        "fftc_execute": ([vp, vp, vp, vp], i32),
+        "fftc_execute_host": ([vp, vp, vp], i32),
+        "fftc_plan_destroy": ([vp], None),
+        "fftc_last_error": ([], i32),
+        "fftc_status_string": ([i32], ctypes.c_char_p),
+        "fftc_plan_describe": ([vp, ctypes.c_char_p, sz], i32),
+        "fftc_plan_launches": ([vp], i32),
+        "fftc_factorize": ([i64, ctypes.POINTER(ctypes.c_int), i32], i32),
+        "fftc_plan_split": ([i64, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)], i32),
+        "fftc_dist_get_unique_id": ([vp], i32),
+        "fftc_dist_plan_create": ([i64, i32, vp, i32, i32, i32], vp),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib
+
+
+# ---------------------------------------------------------------- C names
+def fftc_plan_create(N: int, batch: int, sign: int) -> int:
+    return load().fftc_plan_create(N, batch, sign) or 0
+
+
+def fftc_execute(plan: int, d_in: int, d_out: int, stream: int = 0) -> int:
+    return load().fftc_execute(plan, d_in, d_out, stream)
+
+
+def fftc_execute_host(plan: int, h_in: int, h_out: int) -> int:
+    return load().fftc_execute_host(plan, h_in, h_out)
+
+
+def fftc_plan_destroy(plan: int) -> None:
+    load().fftc_plan_destroy(plan)
+
+
+def fftc_last_error() -> int:
+    return load().fftc_last_error()
+
+
+def fftc_status_string(s: int) -> str:
+    return load().fftc_status_string(s).decode()
+
+
+def fftc_plan_describe(plan: int) -> str:
+    buf = ctypes.create_string_buffer(512)
+    load().fftc_plan_describe(plan, buf, 512)
+    return buf.value.decode()
+
+
+def fftc_plan_launches(plan: int) -> int:
+    return load().fftc_plan_launches(plan)
+
+
+def fftc_factorize(N: int):
+    arr = (ctypes.c_int * 32)()
+    S = load().fftc_factorize(N, arr, 32)
+    return None if S < 0 else [arr[i] for i in range(S)]
+
+
+def fftc_plan_split(N: int):
+    M, K = ctypes.c_int64(), ctypes.c_int64()
+    r = load().fftc_plan_split(N, ctypes.byref(M), ctypes.byref(K))
+    return (r, M.value, K.value)
+
+
+def fftc_dist_get_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(FFTC_NCCL_ID_BYTES)
+    s = load().fftc_dist_get_unique_id(buf)
+    if s != FFTC_SUCCESS:
+        raise FFTCError(s, "fftc_dist_get_unique_id")
+    return buf.raw
+
+
+def fftc_dist_plan_create(N: int, sign: int, nccl_id: bytes | None, rank: int, nranks: int,
+                          loopback: bool = False) -> int:
+    idbuf = ctypes.create_string_buffer(nccl_id, FFTC_NCCL_ID_BYTES) if nccl_id else None
+    return load().fftc_dist_plan_create(N, sign, idbuf, rank, nranks, int(loopback)) or 0
+
+
+# ---------------------------------------------------------------- convenience wrapper
+class Plan:
+    """Owns an fftc plan.  ``plan(x)`` transforms a contiguous complex64 CUDA tensor
+    of ``batch*N`` elements on torch's current stream and returns a new tensor."""
+
+    def __init__(self, N: int, batch: int, sign: int = -1, _handle: int | None = None):
+        self.N, self.batch, self.sign = N, batch, sign
+        self.handle = _handle if _handle is not None else fftc_plan_create(N, batch, sign)
+        if not self.handle:
+            raise FFTCError(fftc_last_error(), "fftc_plan_create(N=%d, batch=%d, sign=%d)" % (N, batch, sign))
+
+    @classmethod
+    def dist(cls, N: int, sign: int, nccl_id: bytes | None, rank: int, nranks: int, loopback: bool = False):
+        h = fftc_dist_plan_create(N, sign, nccl_id, rank, nranks, loopback)
+        if not h:
+            raise FFTCError(fftc_last_error(), "fftc_dist_plan_create(N=%d, P=%d)" % (N, nranks))
+        p = cls.__new__(cls)
+        p.N, p.batch, p.sign, p.handle = N, 1, sign, h
+        return p
+
+    def describe(self) -> str:
+        return fftc_plan_describe(self.handle)
+
+    def launches(self) -> int:
+        return fftc_plan_launches(self.handle)
+
+    def execute(self, x, out, stream=None):
+        import torch
+        if stream is None:
+            stream = torch.cuda.current_stream(x.device).cuda_stream
+        s = fftc_execute(self.handle, x.data_ptr(), out.data_ptr(), stream)
+        if s != FFTC_SUCCESS:
+            raise FFTCError(s, "fftc_execute")
+        return out
+
+    def __call__(self, x, out=None):
+        import torch
+        if x.dtype != torch.complex64 or not x.is_cuda or not x.is_contiguous():
+            raise TypeError("expected a contiguous complex64 CUDA tensor")
+        if out is None:
+            out = torch.empty_like(x)
+        return self.execute(x, out)
+
+    def execute_host(self, x_host, out_host):
+        """End to end on host (ideally pinned) tensors/arrays: H2D, transform, D2H."""
+        s = fftc_execute_host(self.handle, _ptr(x_host), _ptr(out_host))
+        if s != FFTC_SUCCESS:
+            raise FFTCError(s, "fftc_execute_host")
+        return out_host
+
+    def close(self):
+        if getattr(self, "handle", 0):
+            fftc_plan_destroy(self.handle)
+            self.handle = 0
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+def _ptr(a) -> int:
+    if hasattr(a, "data_ptr"):
+        return a.data_ptr()
+    return a.ctypes.data

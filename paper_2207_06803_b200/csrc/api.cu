@@ -1,0 +1,330 @@
+// api.cu -- the C ABI of libfftc.so (include/fftc.h) (product path).
+//
+// Plan creation = planner (planner.cpp) + fp32 twiddle tables computed in double
+// on the host + workspace; execution = stream-ordered kernel launches only.
+// The inverse transform (sign = +1) runs the forward kernels on conjugated
+// input and conjugates the output (IDFT x = conj(DFT(conj x))), so every table
+// and codelet is the forward w_N = exp(-2 pi i / N) of PAPER.md P:46.
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <vector>
+
+#include "../../include/fftc.h"
+#include "dist.h"
+#include "plan.h"
+#include "planner.h"
+
+using namespace fftc;
+
+static thread_local fftc_status g_last = FFTC_SUCCESS;
+
+namespace fftc {
+
+static void root(int64_t e, int64_t L, float2* out) {
+  // w_L^e (forward), exponent reduced mod L in integers, angle taken in double
+  e %= L;
+  if (e < 0) e += L;
+  const double a = 2.0 * M_PI * (double)e / (double)L;
+  out->x = (float)cos(a);
+  out->y = (float)(-sin(a));
+}
+
+float2* upload_stage_table(int64_t N, const int* R, int S, cudaError_t* err) {
+  std::vector<float2> t((size_t)(N > 1 ? N : 1), make_float2(1.f, 0.f));
+  int64_t Ns = 1;
+  for (int s = 0; s < S; ++s) {
+    const int64_t L = Ns * R[s];
+    if (s > 0)
+      for (int r = 1; r < R[s]; ++r)
+        for (int64_t m = 0; m < Ns; ++m) root(m * r, L, &t[(size_t)((Ns - 1) + (r - 1) * Ns + m)]);
+    Ns = L;
+  }
+  float2* d = nullptr;
+  *err = cudaMalloc(&d, t.size() * sizeof(float2));
+  if (*err != cudaSuccess) return nullptr;
+  *err = cudaMemcpy(d, t.data(), t.size() * sizeof(float2), cudaMemcpyHostToDevice);
+  if (*err != cudaSuccess) {
+    cudaFree(d);
+    return nullptr;
+  }
+  return d;
+}
+
+// entries w_N^{h * step} for h < count
+float2* upload_root_table(int64_t N, int64_t count, int64_t step, cudaError_t* err) {
+  std::vector<float2> t((size_t)count);
+  for (int64_t h = 0; h < count; ++h) root(h * step, N, &t[(size_t)h]);
+  float2* d = nullptr;
+  *err = cudaMalloc(&d, t.size() * sizeof(float2));
+  if (*err != cudaSuccess) return nullptr;
+  *err = cudaMemcpy(d, t.data(), t.size() * sizeof(float2), cudaMemcpyHostToDevice);
+  if (*err != cudaSuccess) {
+    cudaFree(d);
+    return nullptr;
+  }
+  return d;
+}
+
+cudaError_t exec_local(const fftc_plan* p, const float2* in, float2* out, long long batch, float2* work,
+                       cudaStream_t st) {
+  const int conj = p->sign > 0;
+  switch (p->kind) {
+    case KIND_COPY:
+      return cudaMemcpyAsync(out, in, (size_t)batch * p->N * sizeof(float2), cudaMemcpyDeviceToDevice, st);
+    case KIND_FUSED:
+      return p->fe->launch(in, out, p->d_tw, batch, conj, st);
+    case KIND_GENERIC:
+      return launch_generic(p->gs, in, out, p->d_tw, batch, conj, st);
+    case KIND_FOURSTEP: {
+      cudaError_t e = p->ce->launch(in, work, p->d_tw, p->d_twA, p->d_twB, (int)p->K, p->N, batch, conj, st);
+      if (e != cudaSuccess) return e;
+      return p->re->launch(work, out, p->d_tw_row, (int)p->M, p->N, batch, conj, st);
+    }
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace fftc
+
+static fftc_status from_cuda(cudaError_t e) {
+  if (e == cudaSuccess) return FFTC_SUCCESS;
+  if (e == cudaErrorMemoryAllocation) return FFTC_ERROR_OUT_OF_MEMORY;
+  if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) return FFTC_ERROR_NO_DEVICE;
+  return FFTC_ERROR_CUDA;
+}
+
+static void free_plan(fftc_plan* p) {
+  if (!p) return;
+  if (p->dist) dist_destroy(p->dist);
+  cudaFree(p->d_tw);
+  cudaFree(p->d_tw_row);
+  cudaFree(p->d_twA);
+  cudaFree(p->d_twB);
+  cudaFree(p->d_work);
+  if (p->hs) {
+    for (int i = 0; i < HostStage::kDepth; ++i) {
+      cudaFree(p->hs->d_in[i]);
+      cudaFree(p->hs->d_out[i]);
+      cudaFree(p->hs->d_work[i]);
+      if (p->hs->st[i]) cudaStreamDestroy(p->hs->st[i]);
+    }
+    delete p->hs;
+  }
+  delete p;
+}
+
+static fftc_plan* fail(fftc_plan* p, fftc_status s) {
+  free_plan(p);
+  g_last = s;
+  return nullptr;
+}
+
+fftc_status fftc_check_device(int* dev) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return FFTC_ERROR_NO_DEVICE;
+  if (cudaGetDevice(dev) != cudaSuccess) return FFTC_ERROR_NO_DEVICE;
+  int major = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, *dev);
+  if (major != 10) return FFTC_ERROR_NO_DEVICE;  // kernels are sm_100a only
+  return FFTC_SUCCESS;
+}
+
+extern "C" {
+
+fftc_plan* fftc_plan_create(int64_t N, int64_t batch, int sign) {
+  g_last = FFTC_SUCCESS;
+  if (N < 1 || batch < 0 || (sign != -1 && sign != 1)) return fail(nullptr, FFTC_ERROR_INVALID_VALUE);
+  if (!seven_smooth(N)) return fail(nullptr, FFTC_ERROR_UNSUPPORTED_SIZE);
+  if (batch > 0 && batch > ((int64_t)1 << 60) / (N * 8)) return fail(nullptr, FFTC_ERROR_UNSUPPORTED_SIZE);
+  int dev = 0;
+  fftc_status ds = fftc_check_device(&dev);
+  if (ds != FFTC_SUCCESS) return fail(nullptr, ds);
+  fftc_plan* p = new fftc_plan();
+  p->N = N;
+  p->batch = batch;
+  p->sign = sign;
+  p->device = dev;
+  cudaError_t err = cudaSuccess;
+  if (N == 1) {
+    p->kind = KIND_COPY;
+    return p;
+  }
+  int64_t M = 0, K = 0;
+  const int split = top_split(N, &M, &K);
+  if (split < 0) return fail(p, FFTC_ERROR_UNSUPPORTED_SIZE);
+  if (split == 1) {
+    int R[kMaxStages];
+    const FusedEntry* fe = find_fused((int)N);
+    if (fe) {
+      p->kind = KIND_FUSED;
+      p->fe = fe;
+      p->d_tw = upload_stage_table(N, fe->R, fe->S, &err);
+    } else {
+      const int S = generic_radices(N, R, kMaxStages);
+      if (S < 0 || S > kMaxStages) return fail(p, FFTC_ERROR_UNSUPPORTED_SIZE);
+      p->kind = KIND_GENERIC;
+      p->gs.N = (int)N;
+      p->gs.S = S;
+      for (int s = 0; s < S; ++s) p->gs.R[s] = R[s];
+      p->d_tw = upload_stage_table(N, R, S, &err);
+    }
+    if (err != cudaSuccess) return fail(p, from_cuda(err));
+    return p;
+  }
+  // four-step
+  p->kind = KIND_FOURSTEP;
+  p->M = M;
+  p->K = K;
+  p->ce = find_col((int)M);
+  p->re = find_row((int)K);
+  if (!p->ce || !p->re) return fail(p, FFTC_ERROR_UNSUPPORTED_SIZE);
+  p->d_tw = upload_stage_table(M, p->ce->R, p->ce->S, &err);
+  if (err == cudaSuccess) p->d_tw_row = upload_stage_table(K, p->re->R, p->re->S, &err);
+  const int64_t nA = N < 4096 ? N : 4096;
+  if (err == cudaSuccess) p->d_twA = upload_root_table(N, nA, 1, &err);
+  if (err == cudaSuccess) p->d_twB = upload_root_table(N, (N + 4095) / 4096, 4096, &err);
+  if (err == cudaSuccess && batch > 0) err = cudaMalloc(&p->d_work, (size_t)(N * batch) * sizeof(float2));
+  if (err != cudaSuccess) return fail(p, from_cuda(err));
+  return p;
+}
+
+static bool misaligned(const void* a) { return ((uintptr_t)a & 15u) != 0; }
+
+fftc_status fftc_execute(const fftc_plan* p, const void* in, void* out, void* stream) {
+  if (!p || !in || !out) return FFTC_ERROR_INVALID_VALUE;
+  if (p->kind == KIND_DIST) return dist_execute(p->dist, in, out, (cudaStream_t)stream);
+  if (p->batch == 0) return FFTC_SUCCESS;
+  const size_t bytes = (size_t)(p->N * p->batch) * sizeof(float2);
+  const char* a = (const char*)in;
+  const char* b = (const char*)out;
+  if (a < b + bytes && b < a + bytes) return FFTC_ERROR_INVALID_VALUE;  // in-place / overlap
+  if (misaligned(in) || misaligned(out)) return FFTC_ERROR_MISALIGNED;
+  cudaError_t e = cudaGetLastError();  // report an earlier asynchronous fault
+  if (e != cudaSuccess) return from_cuda(e);
+  e = exec_local(p, (const float2*)in, (float2*)out, p->batch, p->d_work, (cudaStream_t)stream);
+  return from_cuda(e);
+}
+
+fftc_status fftc_execute_host(fftc_plan* p, const void* host_in, void* host_out) {
+  if (!p || !host_in || !host_out || host_in == host_out) return FFTC_ERROR_INVALID_VALUE;
+  if (p->kind == KIND_DIST) return FFTC_ERROR_INVALID_VALUE;
+  if (p->batch == 0) return FFTC_SUCCESS;
+  const int64_t tbytes = p->N * (int64_t)sizeof(float2);
+  cudaError_t e = cudaSuccess;
+  if (!p->hs) {
+    HostStage* hs = new HostStage();
+    p->hs = hs;
+    // ~32 MiB per chunk, at least one transform
+    int64_t chunk = ((int64_t)32 << 20) / tbytes;
+    if (chunk < 1) chunk = 1;
+    if (chunk > p->batch) chunk = p->batch;
+    hs->chunk = chunk;
+    for (int i = 0; i < HostStage::kDepth && e == cudaSuccess; ++i) {
+      e = cudaMalloc(&hs->d_in[i], (size_t)(chunk * tbytes));
+      if (e == cudaSuccess) e = cudaMalloc(&hs->d_out[i], (size_t)(chunk * tbytes));
+      if (e == cudaSuccess && p->kind == KIND_FOURSTEP) e = cudaMalloc(&hs->d_work[i], (size_t)(chunk * tbytes));
+      if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&hs->st[i], cudaStreamNonBlocking);
+    }
+    if (e != cudaSuccess) return from_cuda(e);
+  }
+  HostStage* hs = p->hs;
+  const char* hin = (const char*)host_in;
+  char* hout = (char*)host_out;
+  int k = 0;
+  for (int64_t t0 = 0; t0 < p->batch && e == cudaSuccess; t0 += hs->chunk, k = (k + 1) % HostStage::kDepth) {
+    const int64_t nb = (p->batch - t0 < hs->chunk) ? p->batch - t0 : hs->chunk;
+    const size_t bytes = (size_t)(nb * tbytes);
+    e = cudaMemcpyAsync(hs->d_in[k], hin + t0 * tbytes, bytes, cudaMemcpyHostToDevice, hs->st[k]);
+    if (e == cudaSuccess) e = exec_local(p, hs->d_in[k], hs->d_out[k], nb, hs->d_work[k], hs->st[k]);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(hout + t0 * tbytes, hs->d_out[k], bytes, cudaMemcpyDeviceToHost, hs->st[k]);
+  }
+  for (int i = 0; i < HostStage::kDepth; ++i) {
+    cudaError_t s = cudaStreamSynchronize(hs->st[i]);
+    if (e == cudaSuccess) e = s;
+  }
+  return from_cuda(e);
+}
+
+void fftc_plan_destroy(fftc_plan* p) { free_plan(p); }
+
+fftc_status fftc_last_error(void) { return g_last; }
+
+const char* fftc_status_string(fftc_status s) {
+  switch (s) {
+    case FFTC_SUCCESS: return "FFTC_SUCCESS";
+    case FFTC_ERROR_INVALID_VALUE: return "FFTC_ERROR_INVALID_VALUE";
+    case FFTC_ERROR_UNSUPPORTED_SIZE: return "FFTC_ERROR_UNSUPPORTED_SIZE";
+    case FFTC_ERROR_MISALIGNED: return "FFTC_ERROR_MISALIGNED";
+    case FFTC_ERROR_OUT_OF_MEMORY: return "FFTC_ERROR_OUT_OF_MEMORY";
+    case FFTC_ERROR_CUDA: return "FFTC_ERROR_CUDA";
+    case FFTC_ERROR_NCCL: return "FFTC_ERROR_NCCL";
+    case FFTC_ERROR_NO_DEVICE: return "FFTC_ERROR_NO_DEVICE";
+  }
+  return "FFTC_UNKNOWN";
+}
+
+int fftc_plan_launches(const fftc_plan* p) {
+  if (!p) return -1;
+  switch (p->kind) {
+    case KIND_COPY: return 0;
+    case KIND_FUSED:
+    case KIND_GENERIC: return p->batch > 0 ? 1 : 0;
+    case KIND_FOURSTEP: return p->batch > 0 ? 2 : 0;
+    case KIND_DIST: return dist_launches(p->dist);
+  }
+  return -1;
+}
+
+int fftc_plan_describe(const fftc_plan* p, char* buf, size_t len) {
+  if (!p) return -1;
+  char tmp[512];
+  int n = 0;
+  auto rad = [&](const int* R, int S) {
+    for (int s = 0; s < S; ++s) n += snprintf(tmp + n, sizeof(tmp) - n, "%s%d", s ? "x" : "", R[s]);
+  };
+  switch (p->kind) {
+    case KIND_COPY:
+      n += snprintf(tmp + n, sizeof(tmp) - n, "kind=copy N=%lld batch=%lld", (long long)p->N, (long long)p->batch);
+      break;
+    case KIND_FUSED:
+      n += snprintf(tmp + n, sizeof(tmp) - n, "kind=fused N=%lld batch=%lld sign=%d radices=", (long long)p->N,
+                    (long long)p->batch, p->sign);
+      rad(p->fe->R, p->fe->S);
+      n += snprintf(tmp + n, sizeof(tmp) - n, " kernel=%s tpf=%d fpb=%d io=%s smem=%zu launches=1", p->fe->name,
+                    p->fe->tpf, p->fe->fpb, p->fe->direct ? "direct" : "staged", p->fe->smem);
+      break;
+    case KIND_GENERIC:
+      n += snprintf(tmp + n, sizeof(tmp) - n, "kind=generic N=%lld batch=%lld sign=%d radices=", (long long)p->N,
+                    (long long)p->batch, p->sign);
+      rad(p->gs.R, p->gs.S);
+      n += snprintf(tmp + n, sizeof(tmp) - n, " launches=1");
+      break;
+    case KIND_FOURSTEP:
+      n += snprintf(tmp + n, sizeof(tmp) - n, "kind=fourstep N=%lld batch=%lld sign=%d M=%lld K=%lld cols=",
+                    (long long)p->N, (long long)p->batch, p->sign, (long long)p->M, (long long)p->K);
+      rad(p->ce->R, p->ce->S);
+      n += snprintf(tmp + n, sizeof(tmp) - n, " rows=");
+      rad(p->re->R, p->re->S);
+      n += snprintf(tmp + n, sizeof(tmp) - n, " workspace=%lld launches=2",
+                    (long long)(p->N * p->batch * (int64_t)sizeof(float2)));
+      break;
+    case KIND_DIST:
+      n += dist_describe(p->dist, tmp + n, sizeof(tmp) - n);
+      break;
+  }
+  if (buf && len) {
+    strncpy(buf, tmp, len - 1);
+    buf[len - 1] = 0;
+  }
+  return n;
+}
+
+int fftc_factorize(int64_t N, int* radices, int max) { return single_pass_radices(N, radices, max); }
+
+int fftc_plan_split(int64_t N, int64_t* M, int64_t* K) { return top_split(N, M, K); }
+
+}  // extern "C"

@@ -1,0 +1,232 @@
+// codelets.cuh -- register-resident DFT_R codelets for sm_100a (product path).
+//
+// A codelet computes y = DFT_R x in registers, natural order in and out, in the
+// forward direction w_R = exp(-2*pi*i/R).  The inverse is
+// obtained by the executor as conj(DFT(conj(x))), so only forward codelets exist.
+//
+// Composite R is built at compile time by the paper's Eq. 2 applied
+// inside the register file:  DFT_R = (DFT_K (x) I_M) D^R_M (I_K (x) DFT_M) Pi^R_K
+// with R = M K: gather at stride K (Pi), M-point codelets on each of the K
+// sub-vectors (I_K (x) DFT_M), twiddles w_R^{r j} at position r M + j (D^R_M),
+// K-point codelets across them (DFT_K (x) I_M).  Trivial twiddles (w^0, +-1,
+// +-i, the eighth roots) are resolved at compile time.  Odd primes use the
+// conjugate-pair symmetric form of the DFT definition.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <type_traits>
+#include <utility>
+
+#ifndef FFTC_HD
+#define FFTC_HD __host__ __device__ __forceinline__
+#endif
+
+namespace fftc {
+
+// ---------------------------------------------------------------- compile-time helpers
+template <int N, int I = 0, class F>
+FFTC_HD void sfor(F&& f) {
+  if constexpr (I < N) {
+    f(std::integral_constant<int, I>{});
+    sfor<N, I + 1>(f);
+  }
+}
+
+constexpr double kPi = 3.14159265358979323846264338327950288;
+
+// Taylor series on [-pi, pi]; 40 terms are far below double rounding there.
+constexpr double taylor_sin(double x) {
+  double term = x, sum = x;
+  for (int n = 1; n < 40; ++n) {
+    term *= -x * x / double((2 * n) * (2 * n + 1));
+    sum += term;
+  }
+  return sum;
+}
+constexpr double taylor_cos(double x) {
+  double term = 1.0, sum = 1.0;
+  for (int n = 1; n < 40; ++n) {
+    term *= -x * x / double((2 * n - 1) * (2 * n));
+    sum += term;
+  }
+  return sum;
+}
+// cos / sin of 2*pi*e/R with the exponent reduced mod R first (exact integer reduction).
+constexpr double cos2pi(long long e, long long R) {
+  e %= R;
+  if (e < 0) e += R;
+  double t = double(e) / double(R);
+  if (t > 0.5) t -= 1.0;
+  return taylor_cos(2.0 * kPi * t);
+}
+constexpr double sin2pi(long long e, long long R) {
+  e %= R;
+  if (e < 0) e += R;
+  double t = double(e) / double(R);
+  if (t > 0.5) t -= 1.0;
+  return taylor_sin(2.0 * kPi * t);
+}
+
+constexpr int smallest_factor(int n) {
+  for (int p = 2; p * p <= n; ++p)
+    if (n % p == 0) return p;
+  return n;
+}
+constexpr bool is_prime(int n) { return n >= 2 && smallest_factor(n) == n; }
+// Outer factor K of a composite codelet R = M*K: prefer 4, then 2, then the smallest prime.
+constexpr int codelet_outer(int R) {
+  if (R % 4 == 0 && R > 4) return 4;
+  return smallest_factor(R);
+}
+
+// ---------------------------------------------------------------- complex helpers
+FFTC_HD float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+FFTC_HD float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+FFTC_HD float2 cmul(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+FFTC_HD float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
+FFTC_HD float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+// -i * a
+FFTC_HD float2 mul_mi(float2 a) { return make_float2(a.y, -a.x); }
+// +i * a
+FFTC_HD float2 mul_pi(float2 a) { return make_float2(-a.y, a.x); }
+
+// a * w_R^E, forward root w_R = exp(-2 pi i / R), E and R compile-time.
+template <int E, int R>
+FFTC_HD float2 mul_root(float2 a) {
+  constexpr int e = ((E % R) + R) % R;
+  if constexpr (e == 0) {
+    return a;
+  } else if constexpr ((8 * e) % R == 0) {
+    constexpr int k8 = (8 * e) / R;  // angle = -k8 * pi / 4
+    constexpr float h = 0.70710678118654752440f;
+    if constexpr (k8 == 2) return mul_mi(a);
+    else if constexpr (k8 == 4) return make_float2(-a.x, -a.y);
+    else if constexpr (k8 == 6) return mul_pi(a);
+    else if constexpr (k8 == 1) return make_float2((a.x + a.y) * h, (a.y - a.x) * h);
+    else if constexpr (k8 == 3) return make_float2((a.y - a.x) * h, -(a.x + a.y) * h);
+    else if constexpr (k8 == 5) return make_float2(-(a.x + a.y) * h, (a.x - a.y) * h);
+    else return make_float2((a.x - a.y) * h, (a.x + a.y) * h);  // k8 == 7
+  } else {
+    constexpr float c = float(cos2pi(e, R));
+    constexpr float s = float(-sin2pi(e, R));
+    return make_float2(fmaf(a.x, c, -a.y * s), fmaf(a.x, s, a.y * c));
+  }
+}
+
+// ---------------------------------------------------------------- codelets
+template <int R, class Enable = void>
+struct Codelet;
+
+template <>
+struct Codelet<1> {
+  FFTC_HD static void run(float2*) {}
+};
+
+template <>
+struct Codelet<2> {
+  FFTC_HD static void run(float2* v) {
+    float2 a = v[0], b = v[1];
+    v[0] = cadd(a, b);
+    v[1] = csub(a, b);
+  }
+};
+
+template <>
+struct Codelet<4> {
+  FFTC_HD static void run(float2* v) {
+    float2 t0 = cadd(v[0], v[2]), t1 = csub(v[0], v[2]);
+    float2 t2 = cadd(v[1], v[3]), t3 = csub(v[1], v[3]);
+    v[0] = cadd(t0, t2);
+    v[2] = csub(t0, t2);
+    v[1] = cadd(t1, mul_mi(t3));
+    v[3] = csub(t1, mul_mi(t3));
+  }
+};
+
+// Odd prime p: symmetric form of the definition y_k = sum_n x_n w_p^{nk}.
+//   A_k = x0 + sum_{n=1}^{h} cos(2 pi n k / p) (x_n + x_{p-n})
+//   B_k =      sum_{n=1}^{h} sin(2 pi n k / p) (x_n - x_{p-n})
+//   y_k = A_k - i B_k,  y_{p-k} = A_k + i B_k        (h = (p-1)/2, forward)
+template <int P>
+struct Codelet<P, std::enable_if_t<(P > 2) && is_prime(P)>> {
+  FFTC_HD static void run(float2* v) {
+    constexpr int h = (P - 1) / 2;
+    float2 sp[h + 1], sm[h + 1];
+    sfor<h>([&](auto n_) {
+      constexpr int n = decltype(n_)::value + 1;
+      sp[n] = cadd(v[n], v[P - n]);
+      sm[n] = csub(v[n], v[P - n]);
+    });
+    float2 y0 = v[0];
+    sfor<h>([&](auto n_) {
+      constexpr int n = decltype(n_)::value + 1;
+      y0 = cadd(y0, sp[n]);
+    });
+    float2 out[P];
+    out[0] = y0;
+    sfor<h>([&](auto k_) {
+      constexpr int k = decltype(k_)::value + 1;
+      float2 A = v[0], B = make_float2(0.f, 0.f);
+      sfor<h>([&](auto n_) {
+        constexpr int n = decltype(n_)::value + 1;
+        constexpr float c = float(cos2pi((long long)n * k, P));
+        constexpr float s = float(sin2pi((long long)n * k, P));
+        A.x = fmaf(c, sp[n].x, A.x);
+        A.y = fmaf(c, sp[n].y, A.y);
+        B.x = fmaf(s, sm[n].x, B.x);
+        B.y = fmaf(s, sm[n].y, B.y);
+      });
+      out[k] = cadd(A, mul_mi(B));
+      out[P - k] = csub(A, mul_mi(B));
+    });
+    sfor<P>([&](auto k_) {
+      constexpr int k = decltype(k_)::value;
+      v[k] = out[k];
+    });
+  }
+};
+
+// Composite R = M*K: Eq. 2 in registers.
+template <int R>
+struct Codelet<R, std::enable_if_t<(R > 4) && !is_prime(R)>> {
+  static constexpr int K = codelet_outer(R);
+  static constexpr int M = R / K;
+  FFTC_HD static void run(float2* v) {
+    float2 u[K][M];
+    // Pi^R_K then I_K (x) DFT_M:  u_r[q] = x[q K + r]
+    sfor<K>([&](auto r_) {
+      constexpr int r = decltype(r_)::value;
+      sfor<M>([&](auto q_) {
+        constexpr int q = decltype(q_)::value;
+        u[r][q] = v[q * K + r];
+      });
+      Codelet<M>::run(u[r]);
+    });
+    // D^R_M: u_r[j] *= w_R^{r j}
+    sfor<K>([&](auto r_) {
+      constexpr int r = decltype(r_)::value;
+      sfor<M>([&](auto j_) {
+        constexpr int j = decltype(j_)::value;
+        u[r][j] = mul_root<r * j, R>(u[r][j]);
+      });
+    });
+    // DFT_K (x) I_M:  X[j + M k1] = sum_r u_r[j] w_K^{r k1}
+    sfor<M>([&](auto j_) {
+      constexpr int j = decltype(j_)::value;
+      float2 w[K];
+      sfor<K>([&](auto r_) {
+        constexpr int r = decltype(r_)::value;
+        w[r] = u[r][j];
+      });
+      Codelet<K>::run(w);
+      sfor<K>([&](auto k_) {
+        constexpr int k1 = decltype(k_)::value;
+        v[j + M * k1] = w[k1];
+      });
+    });
+  }
+};
+
+}  // namespace fftc

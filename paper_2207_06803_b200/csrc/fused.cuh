@@ -1,0 +1,265 @@
+// fused.cuh -- single-pass fused Stockham kernels for sm_100a (product path).
+//
+// One kernel computes whole DFT_N's (N <= 4096) for a tile of FPB transforms:
+// stage-in, S Stockham stages, stage-out; nothing but the input and output
+// touches HBM.  Stage s (radix R, Ns = R_0...R_{s-1}, L = Ns R) is one level of
+// the paper's Eq. 2 with (N -> L, K -> R, M -> Ns):
+//   for each butterfly j in [0, N/R):
+//     v[r]  = a[j + r N/R]                           (Pi folded into the read stride)
+//     v[r] *= w_L^{(j mod Ns) r}        (s > 0)      (D^L_Ns, fp32 table from double)
+//     v     = DFT_R v                                (register codelet, codelets.cuh)
+//     b[(j div Ns) L + (j mod Ns) + r Ns] = v[r]     (Stockham autosort: natural order out)
+// Stages exchange through shared memory in place: every thread first reads all
+// of its butterflies' inputs into registers, the group barrier-syncs, then
+// writes.  Index maps verified against numpy in DESIGN.md §5 / tests.
+//
+// Thread mappings (Map):
+//   LT_FAST: tid = f*TPF + lt -- lanes walk one transform (large N).  Stage 0 can
+//            read HBM directly (coalesced along j) and the last stage can write
+//            HBM directly (coalesced along j).  Shared layout f*N + swz(i), swz an
+//            XOR swizzle of the low 4 bits of i by bits 4..7 (bank-conflict free for
+//            the power-of-two write strides of the autosort).
+//   F_FAST : tid = lt*FPB + f -- lanes walk transforms (small N).  I/O is staged
+//            through shared memory with contiguous 128-bit copies; shared layout
+//            f*(N|1) + i (odd stride -> conflict free across transforms).
+#pragma once
+#include "codelets.cuh"
+
+namespace fftc {
+
+enum Map : int { LT_FAST = 0, F_FAST = 1 };
+
+template <int... Rs>
+struct Radices {
+  static constexpr int S = sizeof...(Rs);
+  static constexpr int R[S] = {Rs...};
+  static constexpr int prod() {
+    int p = 1;
+    for (int s = 0; s < S; ++s) p *= R[s];
+    return p;
+  }
+  static constexpr int ns(int s) {
+    int p = 1;
+    for (int t = 0; t < s; ++t) p *= R[t];
+    return p;
+  }
+};
+
+// Compile-time schedule of one fused transform.
+//   N: length, Rad: Radices<...>, TPF: threads per transform, FPB: transforms per CTA,
+//   MAP: thread mapping, PAD: extra elements per transform row in shared memory
+//   (F_FAST: forced odd stride).
+template <int N_, class Rad, int TPF_, int FPB_, int MAP_, int PAD_ = 0>
+struct Sched {
+  static constexpr int N = N_, TPF = TPF_, FPB = FPB_, MAP = MAP_;
+  static constexpr int S = Rad::S;
+  static constexpr int THREADS = TPF * FPB;
+  static_assert(Rad::prod() == N, "radices must multiply to N");
+  static_assert(THREADS <= 1024, "too many threads");
+  static constexpr int R(int s) { return Rad::R[s]; }
+  static constexpr int ns(int s) { return Rad::ns(s); }
+  static constexpr bool SWZ = (MAP == LT_FAST) && (N % 16 == 0);
+  static constexpr int SS = (MAP == F_FAST) ? ((N + PAD_) | 1) : (N + PAD_);
+  static constexpr size_t SMEM = size_t(SS) * FPB * sizeof(float2);
+  // a transform's threads share one warp -> warp-level barrier suffices
+  static constexpr bool WARP_SYNC = (MAP == LT_FAST) && (TPF <= 32) && (32 % TPF == 0);
+  FFTC_HD static int swz(int i) { return SWZ ? (i ^ ((i >> 4) & 15)) : i; }
+  FFTC_HD static int sidx(int f, int i) { return f * SS + swz(i); }
+  __device__ __forceinline__ static void sync() {
+    if constexpr (WARP_SYNC) __syncwarp();
+    else __syncthreads();
+  }
+  __device__ __forceinline__ static void thread_coords(int tid, int& f, int& lt) {
+    if constexpr (MAP == LT_FAST) {
+      f = tid / TPF;
+      lt = tid % TPF;
+    } else {
+      f = tid % FPB;
+      lt = tid / FPB;
+    }
+  }
+};
+
+// One Stockham stage.  SRC_G: stage reads HBM through gload(i) (else shared);
+// DST_G: stage writes HBM through gstore(i, v) (else shared).
+// Twiddle table layout (per plan, built on the host in double): stage s occupies
+// entries [Ns-1, Ns-1 + (R-1) Ns), entry (Ns-1) + (r-1) Ns + m = w_L^{m r}.
+template <class P, int s, bool SRC_G, bool DST_G, class GL, class GS>
+__device__ __forceinline__ void stage(float2* sm, int f, int lt, bool fvalid,
+                                      const float2* __restrict__ tw, GL&& gload, GS&& gstore) {
+  constexpr int R = P::R(s);
+  constexpr int NB = P::N / R;
+  constexpr int Ns = P::ns(s);
+  constexpr int L = Ns * R;
+  constexpr int KB = (NB + P::TPF - 1) / P::TPF;
+  constexpr bool EXACT = (NB % P::TPF) == 0;
+  float2 v[KB][R];
+  sfor<KB>([&](auto k_) {
+    constexpr int k = decltype(k_)::value;
+    const int j = lt + k * P::TPF;
+    if (fvalid && (EXACT || j < NB)) {
+      sfor<R>([&](auto r_) {
+        constexpr int r = decltype(r_)::value;
+        const int i = j + r * NB;
+        if constexpr (SRC_G) v[k][r] = gload(i);
+        else v[k][r] = sm[P::sidx(f, i)];
+      });
+    }
+  });
+  if constexpr (!SRC_G && !DST_G) P::sync();
+  sfor<KB>([&](auto k_) {
+    constexpr int k = decltype(k_)::value;
+    const int j = lt + k * P::TPF;
+    if (fvalid && (EXACT || j < NB)) {
+      const int m = (Ns == 1) ? 0 : (j % Ns);
+      if constexpr (s > 0) {
+        const float2* t = tw + (Ns - 1) + m;
+        sfor<R - 1>([&](auto r_) {
+          constexpr int r = decltype(r_)::value + 1;
+          v[k][r] = cmul(v[k][r], __ldg(t + (r - 1) * Ns));
+        });
+      }
+      Codelet<R>::run(v[k]);
+      const int o = (Ns == 1) ? j * R : ((j / Ns) * L + m);
+      sfor<R>([&](auto r_) {
+        constexpr int r = decltype(r_)::value;
+        if constexpr (DST_G) gstore(o + r * Ns, v[k][r]);
+        else sm[P::sidx(f, o + r * Ns)] = v[k][r];
+      });
+    }
+  });
+  if constexpr (!DST_G) P::sync();
+}
+
+// All S stages.  SRC0_G: stage 0 reads HBM; DSTL_G: the last stage writes HBM.
+template <class P, bool SRC0_G, bool DSTL_G, class GL, class GS>
+__device__ __forceinline__ void run_stages(float2* sm, int f, int lt, bool fvalid,
+                                           const float2* __restrict__ tw, GL&& gload, GS&& gstore) {
+  sfor<P::S>([&](auto s_) {
+    constexpr int s = decltype(s_)::value;
+    stage<P, s, SRC0_G && s == 0, DSTL_G && s == P::S - 1>(sm, f, lt, fvalid, tw, gload, gstore);
+  });
+}
+
+// Contiguous HBM tile <-> shared (layout P::sidx), 128-bit when the tile base is
+// 16-byte aligned (FPB*N even), element-wise for ragged tails.  csign = -1 applies
+// the conjugation of the inverse transform (IDFT x = conj DFT conj x).
+template <class P>
+__device__ __forceinline__ void tile_in(float2* sm, const float2* __restrict__ g, int nf, float csign) {
+  constexpr int N = P::N;
+  constexpr int TOTAL = P::FPB * N;
+  if constexpr (TOTAL % 2 == 0) {
+    if (nf == P::FPB) {
+      constexpr int PAIRS = TOTAL / 2;
+      constexpr int PER = (PAIRS + P::THREADS - 1) / P::THREADS;
+      const float4* g4 = reinterpret_cast<const float4*>(g);
+      float4 q[PER];
+      sfor<PER>([&](auto k_) {
+        constexpr int k = decltype(k_)::value;
+        const int p = threadIdx.x + k * P::THREADS;
+        if (PAIRS % P::THREADS == 0 || p < PAIRS) q[k] = __ldcs(g4 + p);
+      });
+      sfor<PER>([&](auto k_) {
+        constexpr int k = decltype(k_)::value;
+        const int p = threadIdx.x + k * P::THREADS;
+        if (PAIRS % P::THREADS == 0 || p < PAIRS) {
+          const int e = 2 * p;
+          sm[P::sidx(e / N, e % N)] = make_float2(q[k].x, csign * q[k].y);
+          sm[P::sidx((e + 1) / N, (e + 1) % N)] = make_float2(q[k].z, csign * q[k].w);
+        }
+      });
+      return;
+    }
+  }
+  const int total = nf * N;
+  for (int e = threadIdx.x; e < total; e += P::THREADS) {
+    float2 a = __ldcs(g + e);
+    sm[P::sidx(e / N, e % N)] = make_float2(a.x, csign * a.y);
+  }
+}
+
+template <class P>
+__device__ __forceinline__ void tile_out(const float2* sm, float2* __restrict__ g, int nf, float csign) {
+  constexpr int N = P::N;
+  constexpr int TOTAL = P::FPB * N;
+  if constexpr (TOTAL % 2 == 0) {
+    if (nf == P::FPB) {
+      constexpr int PAIRS = TOTAL / 2;
+      constexpr int PER = (PAIRS + P::THREADS - 1) / P::THREADS;
+      float4* g4 = reinterpret_cast<float4*>(g);
+      sfor<PER>([&](auto k_) {
+        constexpr int k = decltype(k_)::value;
+        const int p = threadIdx.x + k * P::THREADS;
+        if (PAIRS % P::THREADS == 0 || p < PAIRS) {
+          const int e = 2 * p;
+          float2 a = sm[P::sidx(e / N, e % N)];
+          float2 b = sm[P::sidx((e + 1) / N, (e + 1) % N)];
+          __stcs(g4 + p, make_float4(a.x, csign * a.y, b.x, csign * b.y));
+        }
+      });
+      return;
+    }
+  }
+  const int total = nf * N;
+  for (int e = threadIdx.x; e < total; e += P::THREADS) {
+    float2 a = sm[P::sidx(e / N, e % N)];
+    __stcs(g + e, make_float2(a.x, csign * a.y));
+  }
+}
+
+// ---------------------------------------------------------------- batched kernel
+// DIRECT: stage 0 loads HBM and the last stage stores HBM (LT_FAST only);
+// otherwise tile_in / tile_out stage the contiguous FPB*N tile through shared.
+template <class P, bool DIRECT, int MINB>
+__global__ void __launch_bounds__(P::THREADS, MINB)
+    k_fused_batch(const float2* __restrict__ in, float2* __restrict__ out,
+                  const float2* __restrict__ tw, long long batch, float csign) {
+  extern __shared__ float2 sm[];
+  int f, lt;
+  P::thread_coords(threadIdx.x, f, lt);
+  const long long f0 = (long long)blockIdx.x * P::FPB;
+  const long long rem = batch - f0;
+  const int nf = rem < P::FPB ? (int)rem : P::FPB;
+  const bool fvalid = f < nf;
+  const float2* gin = in + f0 * P::N;
+  float2* gout = out + f0 * P::N;
+  if constexpr (DIRECT) {
+    static_assert(P::MAP == LT_FAST, "direct I/O needs the LT_FAST mapping");
+    const float2* gi = gin + (long long)f * P::N;
+    float2* go = gout + (long long)f * P::N;
+    run_stages<P, true, true>(
+        sm, f, lt, fvalid, tw,
+        [&](int i) {
+          float2 a = __ldcs(gi + i);
+          return make_float2(a.x, csign * a.y);
+        },
+        [&](int i, float2 v) { __stcs(go + i, make_float2(v.x, csign * v.y)); });
+  } else {
+    tile_in<P>(sm, gin, nf, csign);
+    __syncthreads();
+    run_stages<P, false, false>(
+        sm, f, lt, fvalid, tw, [&](int) { return make_float2(0.f, 0.f); }, [&](int, float2) {});
+    __syncthreads();
+    tile_out<P>(sm, gout, nf, 1.0f * csign);
+  }
+}
+
+// Host launcher for one compiled schedule.
+template <class P, bool DIRECT, int MINB>
+static cudaError_t launch_fused_batch(const float2* in, float2* out, const float2* tw, long long batch,
+                                      int conj, cudaStream_t st) {
+  auto kern = k_fused_batch<P, DIRECT, MINB>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::SMEM);
+    if (e != cudaSuccess) return e;
+    attr_done = true;
+  }
+  const long long grid = (batch + P::FPB - 1) / P::FPB;
+  if (grid == 0) return cudaSuccess;
+  if (grid > 0x7fffffffLL) return cudaErrorInvalidValue;
+  kern<<<(unsigned)grid, P::THREADS, P::SMEM, st>>>(in, out, tw, batch, conj ? -1.0f : 1.0f);
+  return cudaGetLastError();
+}
+
+}  // namespace fftc

@@ -25,3 +25,11 @@ def pytest_collection_modifyitems(config, items):
     for item in items:
         if "gpu" in item.keywords:
             item.add_marker(skip)
+
+
+def pytest_sessionstart(session):
+    # build the product library and the oracle in-tree if they are missing or stale
+    from paper_2207_06803_b200 import build as _b
+    _b.build()
+    import oracle
+    oracle.build()

@@ -1,0 +1,108 @@
+"""C-ABI boundary and host logic (CPU; no GPU needed).
+
+* libfftc.so loads and exports every function declared in include/fftc.h.
+* The planner (fftc_factorize / fftc_plan_split) obeys SURVEY §8(a) a1: product of
+  radices = N, radices from the codelet set, deterministic, -1 for prime factors > 7.
+* Without a device, plan creation fails loudly (NULL + FFTC_ERROR_NO_DEVICE) -- there
+  is no CPU fallback.
+"""
+import math
+import os
+import re
+import subprocess
+
+import pytest
+
+import paper_2207_06803_b200 as fftc
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _header_functions():
+    txt = open(os.path.join(ROOT, "include", "fftc.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(fftc_[a-z_]+)\s*\(", txt)))
+
+
+def test_library_exports_header_symbols():
+    lib_path = fftc.LIB_PATH
+    assert os.path.exists(lib_path), "libfftc.so must be built (build())"
+    out = subprocess.run(["nm", "-D", "--defined-only", lib_path], capture_output=True, text=True).stdout
+    exported = set(l.split()[-1] for l in out.splitlines() if l.strip())
+    declared = _header_functions()
+    assert len(declared) >= 12
+    missing = [f for f in declared if f not in exported]
+    assert not missing, missing
+    fftc.load()  # dlopen works without a GPU
+
+
+def test_status_strings():
+    for s in range(8):
+        assert fftc.fftc_status_string(s).startswith("FFTC_")
+
+
+def smooth7(n):
+    for p in (2, 3, 5, 7):
+        while n % p == 0:
+            n //= p
+    return n == 1
+
+
+ALLOWED = {2, 3, 4, 5, 7, 8, 9, 10, 14, 15, 16, 25, 27, 32}
+
+
+@pytest.mark.parametrize("N", [n for n in range(1, 4097) if smooth7(n)])
+def test_planner_single_pass(N):
+    R = fftc.fftc_factorize(N)
+    assert R is not None
+    assert math.prod(R) == N
+    assert all(r in ALLOWED for r in R)
+    assert fftc.fftc_factorize(N) == R  # deterministic
+    kind, M, K = fftc.fftc_plan_split(N)
+    assert (kind, M, K) == (1, N, 1)
+
+
+@pytest.mark.parametrize("N", [11, 13, 22, 4097, 17 * 64, 0, -5])
+def test_planner_rejects(N):
+    assert fftc.fftc_factorize(N) is None
+    assert fftc.fftc_plan_split(N)[0] == -1
+
+
+def test_planner_bench_sizes():
+    # SURVEY §8(a) a1 examples (compiled schedules)
+    assert fftc.fftc_factorize(4096) == [16, 16, 16]
+    assert fftc.fftc_factorize(64) == [8, 8]
+    assert fftc.fftc_factorize(60) == [4, 3, 5]
+    assert fftc.fftc_factorize(105) == [3, 5, 7]
+    assert math.prod(fftc.fftc_factorize(2187)) == 2187
+    assert math.prod(fftc.fftc_factorize(3125)) == 3125
+
+
+@pytest.mark.parametrize("N,M,K", [(1 << 16, 256, 256), (1 << 20, 1024, 1024), (1 << 24, 4096, 4096)])
+def test_planner_fourstep_split(N, M, K):
+    assert fftc.fftc_plan_split(N) == (2, M, K)
+    assert math.prod(fftc.fftc_factorize(N)) == N
+
+
+def test_no_device_fails_loudly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    h = fftc.fftc_plan_create(64, 16, -1)
+    assert h == 0
+    assert fftc.fftc_last_error() == fftc.FFTC_ERROR_NO_DEVICE
+    with pytest.raises(fftc.FFTCError):
+        fftc.Plan(64, 16, -1)
+
+
+def test_invalid_args_before_device():
+    # argument validation precedes the device check
+    assert fftc.fftc_plan_create(0, 1, -1) == 0
+    assert fftc.fftc_last_error() == fftc.FFTC_ERROR_INVALID_VALUE
+    assert fftc.fftc_plan_create(8, 1, 0) == 0
+    assert fftc.fftc_last_error() == fftc.FFTC_ERROR_INVALID_VALUE
+    assert fftc.fftc_plan_create(8, -1, -1) == 0
+    assert fftc.fftc_last_error() == fftc.FFTC_ERROR_INVALID_VALUE
+    assert fftc.fftc_plan_create(11, 1, -1) == 0
+    assert fftc.fftc_last_error() == fftc.FFTC_ERROR_UNSUPPORTED_SIZE
+    assert fftc.fftc_execute(0, 0, 0, 0) == fftc.FFTC_ERROR_INVALID_VALUE

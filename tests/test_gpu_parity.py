@@ -1,0 +1,218 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 CPU oracle.
+
+Gate (BASELINE.json north_star): per-transform relative L2 <= 2e-6 * log2(N).
+Inputs are seeded (synth.py); the oracle sees exactly the fp32 array the GPU gets.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+import paper_2207_06803_b200 as fftc  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def gpu_fft(x, sign, N=None):
+    """x: numpy complex64 (batch, N) -> numpy complex64 via fftc (device buffers)."""
+    batch, n = x.shape
+    d = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    with fftc.Plan(n, batch, sign) as p:
+        y = p(d)
+    torch.cuda.synchronize()
+    return y.cpu().numpy()
+
+
+def check(y, x, sign, idx=None, ref="ct"):
+    N = x.shape[1]
+    xs = x if idx is None else x[idx]
+    yr = oracle.fft_ct(xs, sign) if ref == "ct" else oracle.dft_naive(xs, sign)
+    ys = y if idx is None else y[idx]
+    err = oracle.rel_l2(ys, yr)
+    tol = oracle.tolerance(N)
+    assert err.max() <= tol, (N, sign, float(err.max()), tol)
+    # an fp32 FFT sits near 1e-7; 10x that is a bug even when it passes the gate
+    assert err.max() <= 2e-6, (N, sign, float(err.max()))
+    return float(err.max())
+
+
+def sample_idx(batch, seed=0, n_rand=48):
+    rng = np.random.default_rng(seed)
+    idx = set(range(min(8, batch))) | set(range(max(0, batch - 8), batch))
+    if batch > 16:
+        idx |= set(rng.integers(0, batch, n_rand).tolist())
+    return np.array(sorted(idx), dtype=np.int64)
+
+
+POW2 = [1 << k for k in range(3, 13)]
+MIXED = [60, 105, 210, 1000, 2187, 3125]
+GENERIC = [2, 3, 4, 5, 6, 7, 12, 24, 27, 35, 48, 49, 81, 100, 125, 243, 343, 360, 500, 729, 1344, 2401,
+           3000, 3072, 4000]
+
+
+# ---------------------------------------------------------------- config 1
+def test_config1_full():
+    """BASELINE config 1: N=64, batch=4096, U[-1,1) seed 0, forward; every transform."""
+    x = synth.uniform_c64(64, 4096, seed=0)
+    y = gpu_fft(x, -1)
+    check(y, x, -1)
+
+
+# ---------------------------------------------------------------- small batches incl. ragged tails
+@pytest.mark.parametrize("N", POW2 + MIXED + GENERIC)
+@pytest.mark.parametrize("batch", [1, 3, 7, 64])
+@pytest.mark.parametrize("sign", [-1, 1])
+def test_small_batches(N, batch, sign):
+    x = synth.uniform_c64(N, batch, seed=N * 131 + batch)
+    y = gpu_fft(x, sign)
+    check(y, x, sign)
+
+
+@pytest.mark.parametrize("N", [1 << 16, 1 << 20])
+@pytest.mark.parametrize("sign", [-1, 1])
+def test_fourstep_small_batch(N, sign):
+    x = synth.normal_c64(N, 3, seed=N)
+    y = gpu_fft(x, sign)
+    check(y, x, sign)
+
+
+# ---------------------------------------------------------------- full BASELINE sizes (sampled)
+@pytest.mark.parametrize("N", POW2)
+@pytest.mark.parametrize("sign", [-1, 1])
+def test_config2_full_size(N, sign):
+    """BASELINE config 2: batch = 2^26/N; sampled transforms vs O2, plus a whole-buffer Parseval check."""
+    batch = (1 << 26) // N
+    x = synth.uniform_c64(N, batch, seed=0)
+    d = torch.from_numpy(x).cuda()
+    with fftc.Plan(N, batch, sign) as p:
+        yd = p(d)
+    torch.cuda.synchronize()
+    # Parseval over every transform (torch reductions on device: checking, not computing)
+    ex = (d.abs() ** 2).double().sum(dim=1)
+    ey = (yd.abs() ** 2).double().sum(dim=1)
+    rel = ((ey - N * ex).abs() / (N * ex)).max().item()
+    assert rel < 1e-5
+    idx = sample_idx(batch)
+    y = yd[torch.from_numpy(idx).cuda()].cpu().numpy()
+    check(np.asarray(y), x[idx], sign)
+
+
+@pytest.mark.parametrize("N", MIXED)
+def test_config3_full_size(N):
+    batch = (1 << 26) // N
+    x = synth.uniform_c64(N, batch, seed=0)
+    d = torch.from_numpy(x).cuda()
+    with fftc.Plan(N, batch, -1) as p:
+        yd = p(d)
+    torch.cuda.synchronize()
+    idx = sample_idx(batch)
+    y = yd[torch.from_numpy(idx).cuda()].cpu().numpy()
+    check(y, x[idx], -1)
+
+
+@pytest.mark.parametrize("N", [1 << 16, 1 << 20, 1 << 24])
+def test_config4_round_trip(N):
+    """BASELINE config 4: batch = 2^28/N, N(0,1) values; forward then inverse round trip."""
+    batch = (1 << 28) // N
+    x = synth.normal_c64(N, batch, seed=0)
+    d = torch.from_numpy(x).cuda()
+    del x
+    with fftc.Plan(N, batch, -1) as pf, fftc.Plan(N, batch, 1) as pi:
+        yd = pf(d)
+        zd = pi(yd)
+    torch.cuda.synchronize()
+    tol = oracle.tolerance(N)
+    # sampled forward transforms vs O2
+    ns = {1 << 16: 6, 1 << 20: 3, 1 << 24: 1}[N]
+    idx = np.unique(np.array([0, batch - 1] + list(np.random.default_rng(1).integers(0, batch, ns))))
+    xi = d[torch.from_numpy(idx).cuda()].cpu().numpy()
+    yi = yd[torch.from_numpy(idx).cuda()].cpu().numpy()
+    check(yi, xi, -1)
+    # inverse applied to the GPU forward output, vs O2(y_gpu, +1)
+    zi = zd[torch.from_numpy(idx).cuda()].cpu().numpy()
+    zr = oracle.fft_ct(yi, +1)
+    assert oracle.rel_l2(zi, zr).max() <= tol
+    # whole-buffer round trip inv(fwd(x))/N = x
+    num = ((zd / N - d).abs() ** 2).double().sum(dim=1).sqrt()
+    den = (d.abs() ** 2).double().sum(dim=1).sqrt()
+    assert (num / den).max().item() <= 2 * tol
+
+
+# ---------------------------------------------------------------- special inputs
+@pytest.mark.parametrize("N", [8, 64, 60, 105, 1000, 3125, 4096, 1 << 16])
+def test_special_inputs(N):
+    batch = 4
+    d = np.zeros((batch, N), np.complex64)
+    d[:, 0] = 1
+    y = gpu_fft(d, -1)
+    assert np.array_equal(y, np.ones_like(y))  # delta -> exactly ones
+    z = gpu_fft(np.zeros((batch, N), np.complex64), -1)
+    assert np.array_equal(z, np.zeros_like(z))  # zero -> exactly zero
+    k0 = (3 * N) // 7
+    n = np.arange(N)
+    tone = np.exp(2j * np.pi * ((k0 * n) % N) / N).astype(np.complex64)
+    t = gpu_fft(np.tile(tone, (batch, 1)), -1)
+    ref = np.zeros(N); ref[k0] = N
+    assert (np.linalg.norm(t - ref, axis=1) / N).max() <= oracle.tolerance(N)
+    # linearity
+    a = synth.uniform_c64(N, batch, seed=1)
+    b = synth.uniform_c64(N, batch, seed=2)
+    ya, yb = gpu_fft(a, -1), gpu_fft(b, -1)
+    yab = gpu_fft((a + b).astype(np.complex64), -1)
+    assert oracle.rel_l2(yab, ya.astype(np.complex128) + yb).max() <= oracle.tolerance(N)
+
+
+def test_n1_and_batch0():
+    x = synth.uniform_c64(1, 5, seed=0)
+    assert np.array_equal(gpu_fft(x, -1), x)
+    with fftc.Plan(64, 0, -1) as p:
+        t = torch.zeros(16, dtype=torch.complex64, device="cuda")
+        assert fftc.fftc_execute(p.handle, t.data_ptr(), t[8:].data_ptr(), 0) == fftc.FFTC_SUCCESS
+
+
+def test_boundary_errors():
+    N, batch = 64, 16
+    x = torch.zeros(N * batch + 8, dtype=torch.complex64, device="cuda")
+    y = torch.zeros(N * batch + 8, dtype=torch.complex64, device="cuda")
+    with fftc.Plan(N, batch, -1) as p:
+        h = p.handle
+        assert fftc.fftc_execute(h, 0, y.data_ptr(), 0) == fftc.FFTC_ERROR_INVALID_VALUE
+        assert fftc.fftc_execute(h, x.data_ptr(), x.data_ptr(), 0) == fftc.FFTC_ERROR_INVALID_VALUE
+        assert fftc.fftc_execute(h, x.data_ptr(), x.data_ptr() + 8 * 8, 0) == fftc.FFTC_ERROR_INVALID_VALUE
+        assert fftc.fftc_execute(h, x.data_ptr() + 8, y.data_ptr(), 0) == fftc.FFTC_ERROR_MISALIGNED
+        assert fftc.fftc_execute(h, x.data_ptr(), y.data_ptr() + 8, 0) == fftc.FFTC_ERROR_MISALIGNED
+        assert fftc.fftc_execute(h, x.data_ptr(), y.data_ptr(), 0) == fftc.FFTC_SUCCESS
+    for bad, code in [((0, 1, -1), 1), ((8, 1, 0), 1), ((11, 1, -1), 2), ((8 * 13, 1, -1), 2)]:
+        assert fftc.fftc_plan_create(*bad) == 0
+        assert fftc.fftc_last_error() == code
+    torch.cuda.synchronize()
+
+
+def test_describe_and_launches():
+    for N, kind, launches in [(64, "fused", 1), (4096, "fused", 1), (48, "generic", 1), (1 << 20, "fourstep", 2)]:
+        with fftc.Plan(N, 2, -1) as p:
+            assert ("kind=" + kind) in p.describe()
+            assert p.launches() == launches
+
+
+def test_execute_host_matches_device():
+    N, batch = 1000, 2000
+    x = synth.uniform_c64(N, batch, seed=3)
+    out = np.empty_like(x)
+    with fftc.Plan(N, batch, -1) as p:
+        p.execute_host(x, out)
+    y = gpu_fft(x, -1)
+    assert np.array_equal(out, y)  # same kernels, same result bit for bit
+    idx = sample_idx(batch)
+    check(out[idx], x[idx], -1)
+
+
+def test_determinism_bitwise():
+    x = synth.uniform_c64(4096, 256, seed=9)
+    a = gpu_fft(x, -1)
+    b = gpu_fft(x, -1)
+    assert np.array_equal(a, b)
