@@ -61,6 +61,7 @@ __global__ void __launch_bounds__(P::THREADS, MINB)
   const float2* gi = work + b * N + (long long)(j0 + f) * K;
   run_stages<P, true, false>(
       sm, f, lt, true, tw, [&](int i) { return __ldcs(gi + i); }, [&](int, float2) {});
+  __syncthreads();  // the transposed store reads rows written by other warps
   // X[j + M k1] for j in [j0, j0 + FPB): FPB contiguous outputs per k1.
   float2* go = out + b * N + j0;
   static_assert(FPB % 2 == 0, "row tile must hold an even number of rows");

@@ -1,5 +1,6 @@
 """Quick per-size kernel timing (CUDA events, L2 flushed between reps). Dev tool."""
-import sys, json, math
+import sys, json, math, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2207_06803_b200 as fftc
 
