@@ -1,0 +1,337 @@
+#!/usr/bin/env python3
+"""bench.py -- batched 1D C2C FFT on B200 (BASELINE.json metric), one JSON line.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl fftc|reference] [--workload c2|c1|c3|c4]
+
+Workload (default, BASELINE.json configs[1]): the power-of-two sweep
+N = 2^3 ... 2^12, batch = 2^26/N (2^26 complex64 = 512 MiB per buffer, larger
+than the 126 MB L2, so no flush is needed), values U[-1,1) from seed 0, forward
+AND inverse.  One step = the whole sweep = 20 fftc_execute calls (10 sizes x 2
+signs), each a full pass of the hot path (stage-in, Stockham stages, stage-out).
+
+value  = sum over the step of 5 N log2(N) batch flops / device time (GFLOP/s),
+         whole job (all ranks) / max over ranks.
+e2e    = the same metric through fftc_execute_host: pinned host input ->
+         device -> transform -> host output, copies inside the timed region.
+roofline: the fused Stockham kernel family (every launch of the step is one);
+         achieved = algorithmic bytes per launch (16 B per complex element:
+         8 read + 8 written) / mean launch time (CUDA events on
+         the launch stream); peak = MEASURED_PEAKS.json hbm_gbs.
+cpu_baseline: the oracle's recursive Cooley-Tukey (oracle/, fp64, OpenMP) on a
+         bounded sample of the same workload (rank 0, N=1 only).
+
+Multi-GPU (torchrun): every rank runs the full sweep on its own seeded batch
+(weak scaling: transforms are independent, no data-path collective); barrier +
+synchronize around the timed region, max over ranks via all_reduce(MAX).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "batched 1D C2C FFT GFLOP/s (5N·log2N) and HBM GB/s vs peak, 1/2/4/8 B200"
+UNIT = "GFLOP/s"
+ELEMS = 1 << 26
+
+
+def workloads(name):
+    """-> (description, [(N, batch, sign, dist)])"""
+    if name == "c2":
+        jobs = [(1 << k, ELEMS >> k, s, "uniform") for k in range(3, 13) for s in (-1, 1)]
+        return ("C2 pow2 sweep N=2^3..2^12, batch=2^26/N, fwd+inv", jobs)
+    if name == "c1":
+        return ("C1 N=64 batch=4096 fwd", [(64, 4096, -1, "uniform")])
+    if name == "c3":
+        return ("C3 mixed radix N in {60,105,210,1000,2187,3125}, batch=floor(2^26/N), fwd",
+                [(n, ELEMS // n, -1, "uniform") for n in (60, 105, 210, 1000, 2187, 3125)])
+    if name == "c4":
+        return ("C4 four-step N in {2^16,2^20,2^24}, batch=2^28/N, fwd+inv",
+                [(1 << k, (1 << 28) >> k, s, "normal") for k in (16, 20, 24) for s in (-1, 1)])
+    raise ValueError(name)
+
+
+def flops(N, batch):
+    return 5.0 * N * math.log2(N) * batch if N > 1 else 0.0
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("hbm_gbs", 6650.0), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 100 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index=0):
+        self.idx = device_index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.idx), "--query-gpu=" + self.Q,
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([c.strip() for c in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 4 + i and r[4 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ reference arm / cpu baseline
+def oracle_run(jobs, budget_s=15.0, threads=0):
+    """Time the oracle's O2 on a bounded sample of the workload.
+    Returns (GFLOP/s, seconds, sample description, threads)."""
+    import numpy as np
+    import oracle
+    import synth
+    nthreads = threads or len(os.sched_getaffinity(0))
+    # calibration: 2^16 elements of each job, scale the sample to the budget
+    per = []
+    for (N, batch, sign, dist) in jobs:
+        nb = max(1, min(batch, (1 << 16) // N))
+        x = synth.make(dist, N, nb, seed=0)
+        t0 = time.perf_counter()
+        oracle.fft_ct(x, sign, nthreads)
+        per.append((time.perf_counter() - t0) / nb)
+    tot_f, tot_t, parts = 0.0, 0.0, []
+    for (N, batch, sign, dist), pt in zip(jobs, per):
+        # equal time share per job
+        nb = max(1, min(batch, int(budget_s / len(jobs) / max(pt, 1e-9))))
+        x = synth.make(dist, N, nb, seed=0)
+        t0 = time.perf_counter()
+        oracle.fft_ct(x, sign, nthreads)
+        dt = time.perf_counter() - t0
+        tot_f += flops(N, nb)
+        tot_t += dt
+        parts.append("N=%d:%d" % (N, nb))
+    return tot_f / tot_t / 1e9, tot_t, "transforms per job " + ",".join(parts), nthreads
+
+
+# ------------------------------------------------------------------ fftc arm
+def run_fftc(args):
+    import torch
+    import torch.distributed as dist
+    import synth
+    import paper_2207_06803_b200 as fftc
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    dev = torch.device("cuda", local)
+    desc, jobs = workloads(args.workload)
+
+    # inputs: one buffer per distinct (element count, dist); rank r draws its own seeded batch
+    bufs = {}
+    for (N, batch, sign, d) in jobs:
+        key = (N * batch, d, N if d == "normal" else 0)
+        if key not in bufs:
+            x = synth.make(d, N, batch, seed=synth.shard_seed(0, rank))
+            xh = torch.from_numpy(x.reshape(-1)).pin_memory()
+            bufs[key] = (xh, xh.to(dev))
+    maxe = max(N * b for (N, b, _, _) in jobs)
+    out = torch.empty(maxe, dtype=torch.complex64, device=dev)
+    plans = [fftc.Plan(N, b, s) for (N, b, s, _) in jobs]
+    launches_per_step = sum(p.launches() for p in plans)
+    stream = torch.cuda.current_stream(dev)
+
+    def one_step(evs=None):
+        for i, ((N, b, s, d), p) in enumerate(zip(jobs, plans)):
+            x = bufs[(N * b, d, N if d == "normal" else 0)][1]
+            p.execute(x, out)
+            if evs is not None:
+                evs[i + 1].record(stream)
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize(dev)
+
+    K = args.steps
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(len(jobs) + 1)] for _ in range(K)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    sampler = ClockSampler(local)
+    with sampler:
+        for k in range(K):
+            evs[k][0].record(stream)
+            one_step(evs[k])
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    step_ms = [evs[k][0].elapsed_time(evs[k][-1]) for k in range(K)]
+    launch_ms = [[evs[k][i].elapsed_time(evs[k][i + 1]) for i in range(len(jobs))] for k in range(K)]
+    t_rank = sum(step_ms) / 1e3
+    if world > 1:
+        tt = torch.tensor([t_rank], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max = tt.item()
+    else:
+        t_max = t_rank
+    step_flops = sum(flops(N, b) for (N, b, _, _) in jobs)
+    value = world * K * step_flops / t_max / 1e9
+
+    # per-job numbers (rank-local, mean over steps)
+    per_job = []
+    for i, (N, b, s, d) in enumerate(jobs):
+        t = statistics.mean(launch_ms[k][i] for k in range(K)) / 1e3
+        passes = 2 if N > 4096 else 1
+        per_job.append({"N": N, "batch": b, "sign": s, "us": round(t * 1e6, 2),
+                        "gflops": round(flops(N, b) / t / 1e9, 1),
+                        "eff_GBs": round(16 * N * b / t / 1e9, 1), "hbm_passes": passes})
+
+    # roofline over the fused-kernel launches (all single-pass jobs of the step)
+    peak, peak_kind = measured_peaks()
+    sp = [i for i, (N, b, s, d) in enumerate(jobs) if N <= 4096]
+    rl = None
+    if sp:
+        t_mean = statistics.mean(launch_ms[k][i] for k in range(K) for i in sp) / 1e3
+        bytes_mean = statistics.mean(16.0 * jobs[i][0] * jobs[i][1] for i in sp)
+        ach = bytes_mean / t_mean / 1e9
+        traffic = None
+        tf = os.path.join(ROOT, "profiles", "traffic_%s.json" % args.workload)
+        if os.path.exists(tf):
+            traffic = json.load(open(tf)).get("dram_bytes_per_launch")
+        rl = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+              "frac": round(ach / peak, 4), "traffic": traffic,
+              "kernel": "k_fused_batch (fused Stockham, one launch per transform set)",
+              "algorithmic_bytes_per_launch": bytes_mean, "peak_source": peak_kind}
+    clocks = sampler.summary()
+
+    # e2e through the C ABI on host buffers (pinned), H2D + kernels + D2H inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        outs_h = torch.empty(maxe, dtype=torch.complex64).pin_memory()
+        for (N, b, s, d), p in zip(jobs, plans):  # warm the staging buffers
+            p.execute_host(bufs[(N * b, d, N if d == "normal" else 0)][0], outs_h)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        ke = max(1, min(K, 2))
+        for _ in range(ke):
+            for (N, b, s, d), p in zip(jobs, plans):
+                p.execute_host(bufs[(N * b, d, N if d == "normal" else 0)][0], outs_h)
+        te = time.perf_counter() - t0
+        if world > 1:
+            tt = torch.tensor([te], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            te = tt.item()
+        nbytes = sum(8 * N * b for (N, b, _, _) in jobs)
+        e2e = {"value": round(world * ke * step_flops / te / 1e9, 2), "unit": UNIT,
+               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+               "note": "fftc_execute_host, pinned host buffers, 32 MiB chunks over 3 streams"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, t, sample, th = oracle_run(jobs, budget_s=args.cpu_budget)
+        cpu = {"value": round(v, 4), "unit": UNIT, "cores": th, "kind": "oracle",
+               "sample": "O2 recursive Cooley-Tukey fp64 (oracle/oracle.c), %s; %.1f s" % (sample, t)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": round(t_max * 1e3 / K, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32 (complex64)",
+            "data": "synthetic: re/im U[-1,1) (normal for C4), numpy PCG64 seed 0 (rank r: SeedSequence [0,r])",
+            "config": {"workload": desc, "elements_per_transform_set": maxe,
+                       "transform_sets_per_step": len(jobs), "l2": "inputs 512 MiB > 126 MB L2, no flush",
+                       "parallelism": "batch-sharded weak scaling x%d" % world},
+            "roofline": rl, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_per_step * K,
+            "clocks": clocks, "per_job": per_job,
+        }
+        print(json.dumps(line), flush=True)
+    for p in plans:
+        p.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    desc, jobs = workloads(args.workload)
+    # each step: a bounded sample of the workload on the host cores (oracle as it stands)
+    for _ in range(args.warmup):
+        oracle_run(jobs[:1], budget_s=0.2)
+    vals, ts, sample, th = [], 0.0, "", 0
+    for _ in range(args.steps):
+        v, t, sample, th = oracle_run(jobs, budget_s=min(args.ref_budget, 150.0 / max(1, args.steps)))
+        vals.append(v)
+        ts += t
+    value = statistics.mean(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ts * 1e3 / args.steps, 2),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic, same seeds as the fftc arm",
+            "config": {"workload": desc, "sample": sample},
+            "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": th, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="fftc", choices=["fftc", "reference"])
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--ref-budget", type=float, default=10.0)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "fftc":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_fftc(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -123,7 +123,13 @@ fftc_plan* fftc_dist_plan_create(int64_t N, int sign, const void* nccl_id, int r
                                  int loopback);
 
 /* fftc_execute on a distributed plan: in / out are this rank's
- * N/nranks-element natural-order slabs (device). */
+ * N/nranks-element natural-order slabs (device); in loopback mode the whole
+ * N-element vectors.  Enqueues 4-5 kernels and 3 all-to-alls per call. */
+
+/* Host only (no device): the split the six-step uses for (N, nranks):
+ * out[0..3] = M, K, K1, K2 (K = K1*K2; K2 == 1 when DFT_K is single pass).
+ * Returns 0, or -1 if no supported split exists.                           */
+int fftc_dist_split(int64_t N, int nranks, int64_t* out4);
 
 #ifdef __cplusplus
 }

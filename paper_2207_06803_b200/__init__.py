@@ -9,7 +9,7 @@ Functions keep the C names (``fftc_plan_create``, ``fftc_execute``,
 ``fftc_execute_host``, ``fftc_plan_destroy``, ``fftc_last_error``,
 ``fftc_status_string``, ``fftc_plan_describe``, ``fftc_plan_launches``,
 ``fftc_factorize``, ``fftc_plan_split``, ``fftc_dist_get_unique_id``,
-``fftc_dist_plan_create``); :class:`Plan` is a convenience wrapper that owns a
+``fftc_dist_plan_create``, ``fftc_dist_split``); :class:`Plan` is a convenience wrapper that owns a
 plan handle and takes contiguous ``torch.complex64`` CUDA tensors.
 """
 from __future__ import annotations
@@ -62,6 +62,7 @@ def load(path: str = LIB_PATH):
         "fftc_plan_split": ([i64, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)], i32),
         "fftc_dist_get_unique_id": ([vp], i32),
         "fftc_dist_plan_create": ([i64, i32, vp, i32, i32, i32], vp),
+        "fftc_dist_split": ([i64, i32, ctypes.POINTER(ctypes.c_int64)], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -116,6 +117,12 @@ def fftc_plan_split(N: int):
     M, K = ctypes.c_int64(), ctypes.c_int64()
     r = load().fftc_plan_split(N, ctypes.byref(M), ctypes.byref(K))
     return (r, M.value, K.value)
+
+
+def fftc_dist_split(N: int, nranks: int):
+    out = (ctypes.c_int64 * 4)()
+    r = load().fftc_dist_split(N, nranks, out)
+    return None if r != 0 else tuple(out[i] for i in range(4))
 
 
 def fftc_dist_get_unique_id() -> bytes:

@@ -78,7 +78,8 @@ cudaError_t exec_local(const fftc_plan* p, const float2* in, float2* out, long l
     case KIND_GENERIC:
       return launch_generic(p->gs, in, out, p->d_tw, batch, conj, st);
     case KIND_FOURSTEP: {
-      cudaError_t e = p->ce->launch(in, work, p->d_tw, p->d_twA, p->d_twB, (int)p->K, p->N, batch, conj, st);
+      const ColGeom g = fourstep_cols_geom(p->ce, p->N, p->K);
+      cudaError_t e = p->ce->launch(in, work, p->d_tw, p->d_twA, p->d_twB, g, batch, conj, 0, st);
       if (e != cudaSuccess) return e;
       return p->re->launch(work, out, p->d_tw_row, (int)p->M, p->N, batch, conj, st);
     }
@@ -122,7 +123,9 @@ static fftc_plan* fail(fftc_plan* p, fftc_status s) {
   return nullptr;
 }
 
-fftc_status fftc_check_device(int* dev) {
+extern "C" void fftc_set_last_error(fftc_status s) { g_last = s; }
+
+extern "C" fftc_status fftc_check_device(int* dev) {
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return FFTC_ERROR_NO_DEVICE;
   if (cudaGetDevice(dev) != cudaSuccess) return FFTC_ERROR_NO_DEVICE;

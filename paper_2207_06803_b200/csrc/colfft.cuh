@@ -1,0 +1,98 @@
+// colfft.cuh -- strided "column" DFT_L kernel (product path).
+//
+// The large-N paths apply Eq. 2 at the top level with both factors
+// large; each factor is a batch of DFT_L's along a strided axis of a 2D view
+// ("columns").  k_colx computes DFT_L down C adjacent columns per CTA (columns are
+// unit-stride apart, so a warp reads C*8-byte contiguous segments), with the inner
+// DFT_L a fused Stockham pass (fused.cuh, F_FAST mapping: lanes walk columns).
+//
+// Geometry (runtime, ColGeom): column c = grp * G + ci (ci < G = tiles * C);
+//   input  element i : in  + grp*in_g  + ci + i*in_s
+//   output element k : out + grp*out_g + ci*out_c + (k >> ocl)*out_cs + (k & omask)*out_s
+//   optional twiddle : y_k *= w_T^{((ci >> tw_shift) + tw_off) * k}   (T-point root,
+//                      read as A[e mod 4096] * B[e div 4096] from two fp32 tables)
+// OUT_T = false: the last stage stores HBM directly (lanes walk columns; needs out_c = 1).
+// OUT_T = true : the last stage stores shared memory, then a cooperative store walks k
+//                (lanes walk the transform), for outputs whose columns are far apart
+//                (the six-step's chunked layouts).
+#pragma once
+#include "colgeom.h"
+#include "fused.cuh"
+
+namespace fftc {
+
+
+template <class P, bool OUT_T, int MINB>
+__global__ void __launch_bounds__(P::THREADS, MINB)
+    k_colx(const float2* __restrict__ in, float2* __restrict__ out, const float2* __restrict__ tw,
+           const float2* __restrict__ twA, const float2* __restrict__ twB, ColGeom g, float csign_in,
+           float csign_out) {
+  extern __shared__ float2 sm[];
+  static_assert(P::MAP == F_FAST, "column kernel walks columns");
+  constexpr int L = P::N;
+  constexpr int C = P::FPB;
+  int f, lt;
+  P::thread_coords(threadIdx.x, f, lt);
+  const long long grp = blockIdx.x / g.tiles;
+  const int ci0 = (blockIdx.x % g.tiles) * C;
+  const int ci = ci0 + f;
+  const float2* gi = in + grp * g.in_g + ci;
+  const long long omask = (1LL << g.ocl) - 1;
+  auto twiddle = [&](int cc, int k, float2 v) {
+    if (g.tw) {
+      const long long e = ((long long)(cc >> g.tw_shift) + g.tw_off) * k;
+      const float2 w = cmul(__ldg(twA + (e & 4095)), __ldg(twB + (e >> 12)));
+      v = cmul(v, w);
+    }
+    return v;
+  };
+  auto load = [&](int i) {
+    float2 a = __ldcs(gi + (long long)i * g.in_s);
+    return make_float2(a.x, csign_in * a.y);
+  };
+  if constexpr (!OUT_T) {
+    float2* go = out + grp * g.out_g + ci * g.out_c;
+    run_stages<P, true, true>(sm, f, lt, true, tw, load, [&](int k, float2 v) {
+      v = twiddle(ci, k, v);
+      __stcs(go + ((long long)k >> g.ocl) * g.out_cs + ((long long)k & omask) * g.out_s,
+             make_float2(v.x, csign_out * v.y));
+    });
+  } else {
+    run_stages<P, true, false>(sm, f, lt, true, tw, load, [&](int, float2) {});
+    __syncthreads();
+    float2* go = out + grp * g.out_g;
+    constexpr int TOTAL = L * C;
+    static_assert(TOTAL % P::THREADS == 0, "tile must split evenly");
+    constexpr int PER = TOTAL / P::THREADS;
+    sfor<PER>([&](auto n_) {
+      constexpr int n = decltype(n_)::value;
+      const int e = threadIdx.x + n * P::THREADS;
+      const int k = e % L, cc = e / L;
+      float2 v = twiddle(ci0 + cc, k, sm[P::sidx(cc, k)]);
+      __stcs(go + (long long)(ci0 + cc) * g.out_c + ((long long)k >> g.ocl) * g.out_cs +
+                 ((long long)k & omask) * g.out_s,
+             make_float2(v.x, csign_out * v.y));
+    });
+  }
+}
+
+template <class P, bool OUT_T, int MINB>
+static cudaError_t launch_colx(const float2* in, float2* out, const float2* tw, const float2* twA,
+                               const float2* twB, const ColGeom& g, long long groups, int conj_in,
+                               int conj_out, cudaStream_t st) {
+  auto kern = k_colx<P, OUT_T, MINB>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const long long grid = groups * g.tiles;
+  if (grid == 0) return cudaSuccess;
+  if (grid > 0x7fffffffLL) return cudaErrorInvalidValue;
+  kern<<<(unsigned)grid, P::THREADS, P::SMEM, st>>>(in, out, tw, twA, twB, g, conj_in ? -1.f : 1.f,
+                                                    conj_out ? -1.f : 1.f);
+  return cudaGetLastError();
+}
+
+}  // namespace fftc

@@ -1,0 +1,20 @@
+// colgeom.h -- geometry of a strided column DFT launch (see colfft.cuh) (product path).
+#pragma once
+
+namespace fftc {
+
+struct ColGeom {
+  int tiles;         // column tiles (of C) per group
+  long long in_g;    // input offset between groups
+  long long in_s;    // input stride along the transform
+  long long out_g;   // output offset between groups
+  long long out_c;   // output stride between columns
+  long long out_s;   // output stride along the transform (within a chunk)
+  long long out_cs;  // output offset between chunks of (omask+1) outputs
+  int ocl;           // log2 of the output chunk length (>= 30: no chunking)
+  int tw;            // apply the twiddle
+  int tw_shift;      // twiddle column index = (ci >> tw_shift) + tw_off
+  long long tw_off;
+};
+
+}  // namespace fftc

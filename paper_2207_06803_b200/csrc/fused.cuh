@@ -29,6 +29,12 @@ namespace fftc {
 
 enum Map : int { LT_FAST = 0, F_FAST = 1 };
 
+constexpr int highbit(int r) {
+  int h = 1;
+  while (h * 2 <= r) h *= 2;
+  return h;
+}
+
 template <int... Rs>
 struct Radices {
   static constexpr int S = sizeof...(Rs);
@@ -45,11 +51,25 @@ struct Radices {
   }
 };
 
+// Shared-memory layouts of a tile of FPB transforms (element i of transform f):
+//   LAY_SWZ  : f*SS + swz(i), swz XORs bits 0..3 of i with bits 4..7 (LT_FAST; lanes
+//              of a 16-lane phase walk one transform; power-of-two autosort strides).
+//   LAY_FXOR : f*N + (i ^ gf(f)) (F_FAST, N % 16 == 0 or N == 8; lanes walk f).
+//   LAY_ODD  : f*SS + i, SS odd (F_FAST, other N).
+//   LAY_INTER: swzc(i)*FPB + f (interleaved columns, F_FAST with FPB < 16: a phase
+//              holds FPB columns x 16/FPB consecutive butterflies).
+enum Layout : int { LAY_AUTO = -1, LAY_SWZ = 0, LAY_FXOR = 1, LAY_ODD = 2, LAY_INTER = 3 };
+
+constexpr int ilog2(int n) {
+  int l = 0;
+  while ((1 << (l + 1)) <= n) ++l;
+  return l;
+}
+
 // Compile-time schedule of one fused transform.
 //   N: length, Rad: Radices<...>, TPF: threads per transform, FPB: transforms per CTA,
-//   MAP: thread mapping, PAD: extra elements per transform row in shared memory
-//   (F_FAST: forced odd stride).
-template <int N_, class Rad, int TPF_, int FPB_, int MAP_, int PAD_ = 0>
+//   MAP: thread mapping, PAD: extra elements per transform row (LAY_SWZ / LAY_ODD).
+template <int N_, class Rad, int TPF_, int FPB_, int MAP_, int PAD_ = 0, int LAY_ = LAY_AUTO>
 struct Sched {
   static constexpr int N = N_, TPF = TPF_, FPB = FPB_, MAP = MAP_;
   static constexpr int S = Rad::S;
@@ -58,13 +78,25 @@ struct Sched {
   static_assert(THREADS <= 1024, "too many threads");
   static constexpr int R(int s) { return Rad::R[s]; }
   static constexpr int ns(int s) { return Rad::ns(s); }
-  static constexpr bool SWZ = (MAP == LT_FAST) && (N % 16 == 0);
-  static constexpr int SS = (MAP == F_FAST) ? ((N + PAD_) | 1) : (N + PAD_);
-  static constexpr size_t SMEM = size_t(SS) * FPB * sizeof(float2);
+  static constexpr int LAY = (LAY_ != LAY_AUTO) ? LAY_
+                             : (MAP == LT_FAST) ? LAY_SWZ
+                             : (PAD_ == 0 && (N % 16 == 0 || N == 8)) ? LAY_FXOR : LAY_ODD;
+  static constexpr bool FXOR = (LAY == LAY_FXOR);
+  static constexpr bool SWZ = (LAY == LAY_SWZ) && (N % 16 == 0);
+  static constexpr int SS = (LAY == LAY_FXOR) ? N : (LAY == LAY_ODD) ? ((N + PAD_) | 1) : (N + PAD_);
+  static constexpr size_t SMEM = size_t(LAY == LAY_INTER ? N : SS) * FPB * sizeof(float2);
+  // LAY_INTER: XOR the bank bits of i (mod 16/FPB) with the bits above the leaf radix
+  static constexpr int IMASK = (LAY == LAY_INTER && FPB < 16) ? (16 / FPB - 1) : 0;
+  static constexpr int ISHIFT = ilog2(Rad::R[0]);
   // a transform's threads share one warp -> warp-level barrier suffices
   static constexpr bool WARP_SYNC = (MAP == LT_FAST) && (TPF <= 32) && (32 % TPF == 0);
   FFTC_HD static int swz(int i) { return SWZ ? (i ^ ((i >> 4) & 15)) : i; }
-  FFTC_HD static int sidx(int f, int i) { return f * SS + swz(i); }
+  FFTC_HD static int gf(int f) { return (N % 16 == 0) ? (f & 15) : ((f >> 1) & 7); }
+  FFTC_HD static int sidx(int f, int i) {
+    if constexpr (LAY == LAY_FXOR) return f * SS + (i ^ gf(f));
+    else if constexpr (LAY == LAY_INTER) return (i ^ ((i >> ISHIFT) & IMASK)) * FPB + f;
+    else return f * SS + swz(i);
+  }
   __device__ __forceinline__ static void sync() {
     if constexpr (WARP_SYNC) __syncwarp();
     else __syncthreads();
@@ -113,10 +145,16 @@ __device__ __forceinline__ void stage(float2* sm, int f, int lt, bool fvalid,
     if (fvalid && (EXACT || j < NB)) {
       const int m = (Ns == 1) ? 0 : (j % Ns);
       if constexpr (s > 0) {
+        // w_L^{m r}: table loads for r = 1, 2, 4, 8, ...; every other r as the product
+        // w^{2^b} w^{r - 2^b} (at most log2(R)-1 roundings deep)
         const float2* t = tw + (Ns - 1) + m;
+        float2 w[R];
         sfor<R - 1>([&](auto r_) {
           constexpr int r = decltype(r_)::value + 1;
-          v[k][r] = cmul(v[k][r], __ldg(t + (r - 1) * Ns));
+          constexpr int hb = highbit(r);
+          if constexpr (hb == r) w[r] = __ldg(t + (r - 1) * Ns);
+          else w[r] = cmul(w[hb], w[r - hb]);
+          v[k][r] = cmul(v[k][r], w[r]);
         });
       }
       Codelet<R>::run(v[k]);
@@ -148,7 +186,31 @@ template <class P>
 __device__ __forceinline__ void tile_in(float2* sm, const float2* __restrict__ g, int nf, float csign) {
   constexpr int N = P::N;
   constexpr int TOTAL = P::FPB * N;
-  if constexpr (TOTAL % 2 == 0) {
+  if constexpr (P::FXOR) {
+    // 128-bit loads, 128-bit stores into the XOR layout (pairs stay aligned, maybe swapped)
+    if (nf == P::FPB) {
+      constexpr int PAIRS = TOTAL / 2;
+      constexpr int PER = (PAIRS + P::THREADS - 1) / P::THREADS;
+      const float4* g4 = reinterpret_cast<const float4*>(g);
+      float4 q[PER];
+      sfor<PER>([&](auto k_) {
+        constexpr int k = decltype(k_)::value;
+        const int p = threadIdx.x + k * P::THREADS;
+        if (PAIRS % P::THREADS == 0 || p < PAIRS) q[k] = __ldcs(g4 + p);
+      });
+      sfor<PER>([&](auto k_) {
+        constexpr int k = decltype(k_)::value;
+        const int p = threadIdx.x + k * P::THREADS;
+        if (PAIRS % P::THREADS == 0 || p < PAIRS) {
+          const int e = 2 * p, f = e / N, i = e % N, gx = P::gf(f);
+          float4 v = make_float4(q[k].x, csign * q[k].y, q[k].z, csign * q[k].w);
+          if (gx & 1) v = make_float4(v.z, v.w, v.x, v.y);
+          *reinterpret_cast<float4*>(sm + f * N + ((i ^ gx) & ~1)) = v;
+        }
+      });
+      return;
+    }
+  } else if constexpr (TOTAL % 2 == 0 && P::MAP == LT_FAST) {
     if (nf == P::FPB) {
       constexpr int PAIRS = TOTAL / 2;
       constexpr int PER = (PAIRS + P::THREADS - 1) / P::THREADS;
@@ -170,6 +232,23 @@ __device__ __forceinline__ void tile_in(float2* sm, const float2* __restrict__ g
       });
       return;
     }
+  } else {
+    // odd shared stride: element-wise (consecutive lanes -> consecutive banks)
+    if (nf == P::FPB) {
+      constexpr int PER = (TOTAL + P::THREADS - 1) / P::THREADS;
+      float2 q[PER];
+      sfor<PER>([&](auto k_) {
+        constexpr int k = decltype(k_)::value;
+        const int e = threadIdx.x + k * P::THREADS;
+        if (TOTAL % P::THREADS == 0 || e < TOTAL) q[k] = __ldcs(g + e);
+      });
+      sfor<PER>([&](auto k_) {
+        constexpr int k = decltype(k_)::value;
+        const int e = threadIdx.x + k * P::THREADS;
+        if (TOTAL % P::THREADS == 0 || e < TOTAL) sm[P::sidx(e / N, e % N)] = make_float2(q[k].x, csign * q[k].y);
+      });
+      return;
+    }
   }
   const int total = nf * N;
   for (int e = threadIdx.x; e < total; e += P::THREADS) {
@@ -182,7 +261,24 @@ template <class P>
 __device__ __forceinline__ void tile_out(const float2* sm, float2* __restrict__ g, int nf, float csign) {
   constexpr int N = P::N;
   constexpr int TOTAL = P::FPB * N;
-  if constexpr (TOTAL % 2 == 0) {
+  if constexpr (P::FXOR) {
+    if (nf == P::FPB) {
+      constexpr int PAIRS = TOTAL / 2;
+      constexpr int PER = (PAIRS + P::THREADS - 1) / P::THREADS;
+      float4* g4 = reinterpret_cast<float4*>(g);
+      sfor<PER>([&](auto k_) {
+        constexpr int k = decltype(k_)::value;
+        const int p = threadIdx.x + k * P::THREADS;
+        if (PAIRS % P::THREADS == 0 || p < PAIRS) {
+          const int e = 2 * p, f = e / N, i = e % N, gx = P::gf(f);
+          float4 v = *reinterpret_cast<const float4*>(sm + f * N + ((i ^ gx) & ~1));
+          if (gx & 1) v = make_float4(v.z, v.w, v.x, v.y);
+          __stcs(g4 + p, make_float4(v.x, csign * v.y, v.z, csign * v.w));
+        }
+      });
+      return;
+    }
+  } else if constexpr (TOTAL % 2 == 0 && P::MAP == LT_FAST) {
     if (nf == P::FPB) {
       constexpr int PAIRS = TOTAL / 2;
       constexpr int PER = (PAIRS + P::THREADS - 1) / P::THREADS;
@@ -195,6 +291,19 @@ __device__ __forceinline__ void tile_out(const float2* sm, float2* __restrict__ 
           float2 a = sm[P::sidx(e / N, e % N)];
           float2 b = sm[P::sidx((e + 1) / N, (e + 1) % N)];
           __stcs(g4 + p, make_float4(a.x, csign * a.y, b.x, csign * b.y));
+        }
+      });
+      return;
+    }
+  } else {
+    if (nf == P::FPB) {
+      constexpr int PER = (TOTAL + P::THREADS - 1) / P::THREADS;
+      sfor<PER>([&](auto k_) {
+        constexpr int k = decltype(k_)::value;
+        const int e = threadIdx.x + k * P::THREADS;
+        if (TOTAL % P::THREADS == 0 || e < TOTAL) {
+          float2 a = sm[P::sidx(e / N, e % N)];
+          __stcs(g + e, make_float2(a.x, csign * a.y));
         }
       });
       return;
