@@ -54,6 +54,9 @@ def workloads(name):
     if name == "c3":
         return ("C3 mixed radix N in {60,105,210,1000,2187,3125}, batch=floor(2^26/N), fwd",
                 [(n, ELEMS // n, -1, "uniform") for n in (60, 105, 210, 1000, 2187, 3125)])
+    if name == "c5":
+        return ("C5 distributed six-step N=2^30, one transform, block-distributed over the ranks, fwd",
+                [(1 << 30, 1, -1, "uniform")])
     if name == "c4":
         return ("C4 four-step N in {2^16,2^20,2^24}, batch=2^28/N, fwd+inv",
                 [(1 << k, (1 << 28) >> k, s, "normal") for k in (16, 20, 24) for s in (-1, 1)])
@@ -73,32 +76,49 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 100 ms during the timed region."""
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    """SM clock + throttle reasons sampled through NVML every 2 ms during the timed region."""
 
-    def __init__(self, device_index=0):
+    def __init__(self, device_index=0, period=0.002):
         self.idx = device_index
-        self.rows = []
+        self.period = period
+        self.sm, self.mx, self.reasons = [], [], set()
         self._stop = threading.Event()
         self._t = None
+        self.ok = False
 
     def _run(self):
-        while not self._stop.is_set():
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = None
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.idx), "--query-gpu=" + self.Q,
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([c.strip() for c in out.split(",")])
+                import torch
+                uuid = str(torch.cuda.get_device_properties(self.idx).uuid)
+                h = nv.nvmlDeviceGetHandleByUUID(("GPU-" + uuid).encode())
             except Exception:
-                pass
-            self._stop.wait(0.1)
+                h = nv.nvmlDeviceGetHandleByIndex(self.idx)
+            bits = {"hw_slowdown": nv.nvmlClocksThrottleReasonHwSlowdown,
+                    "hw_thermal_slowdown": getattr(nv, "nvmlClocksThrottleReasonHwThermalSlowdown", 0x40),
+                    "sw_thermal_slowdown": getattr(nv, "nvmlClocksThrottleReasonSwThermalSlowdown", 0x20),
+                    "sw_power_cap": nv.nvmlClocksThrottleReasonSwPowerCap}
+            self.mx.append(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            self.ok = True
+            while True:
+                self.sm.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                for name, b in bits.items():
+                    if r & b:
+                        self.reasons.add(name)
+                if self._stop.wait(self.period):
+                    break
+            nv.nvmlShutdown()
+        except Exception as e:  # pragma: no cover
+            self.reasons.add("nvml unavailable: %s" % type(e).__name__)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
+        time.sleep(0.01)
         return self
 
     def __exit__(self, *a):
@@ -106,14 +126,9 @@ class ClockSampler:
         self._t.join(timeout=10)
 
     def summary(self):
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 4 + i and r[4 + i] == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        return {"sm_mhz": statistics.median(self.sm) if self.sm else None,
+                "sm_max_mhz": max(self.mx) if self.mx else None,
+                "reasons": sorted(self.reasons), "samples": len(self.sm)}
 
 
 # ------------------------------------------------------------------ reference arm / cpu baseline
@@ -287,6 +302,70 @@ def run_fftc(args):
         dist.destroy_process_group()
 
 
+def run_c5(args):
+    """Six-step over WORLD_SIZE ranks (NCCL all-to-alls); one rank = the same six-step on one GPU."""
+    import torch
+    import torch.distributed as dist
+    import synth
+    import paper_2207_06803_b200 as fftc
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    N = args.c5_n
+    if world > 1:
+        dist.init_process_group("nccl")
+        idt = torch.zeros(fftc.FFTC_NCCL_ID_BYTES, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(fftc.fftc_dist_get_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        nid = bytes(idt.cpu().numpy().tobytes())
+    else:
+        nid = None
+    plan = fftc.Plan.dist(N, -1, nid, rank, world)
+    slab = N // world
+    # rank r holds elements [r N/P, (r+1) N/P) of one seeded U[-1,1) vector (generated per slab
+    # from a per-rank seed so no rank materialises the whole 8 GiB vector)
+    x = torch.from_numpy(synth.uniform_c64(slab, 1, seed=synth.shard_seed(0, rank))[0]).to(dev)
+    y = torch.empty_like(x)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        plan.execute(x, y)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    K = args.steps
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local)
+    with sampler:
+        e0.record(stream)
+        for _ in range(K):
+            plan.execute(x, y)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+    t = e0.elapsed_time(e1) / 1e3
+    if world > 1:
+        tt = torch.tensor([t], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = tt.item()
+    value = K * flops(N, 1) / t / 1e9
+    if rank == 0:
+        a2a_bytes = 3 * (world - 1) / world * 8 * N / world if world > 1 else 0
+        line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": K,
+                "warmup": args.warmup, "ms_per_step": round(t * 1e3 / K, 4), "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32 (complex64)",
+                "data": "synthetic U[-1,1), per-rank seeded slabs",
+                "config": {"workload": "C5 six-step N=%d over %d rank(s)" % (N, world), "plan": plan.describe(),
+                           "nvlink_bytes_per_rank_per_step": a2a_bytes},
+                "gpu_launches": plan.launches() * K, "clocks": sampler.summary()}
+        print(json.dumps(line), flush=True)
+    plan.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def run_reference(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -316,10 +395,11 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="fftc", choices=["fftc", "reference"])
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--c5-n", type=int, default=1 << 30)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
@@ -329,6 +409,8 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload == "c5":
+        run_c5(args)
     else:
         run_fftc(args)
 

@@ -94,6 +94,13 @@ int fftc_plan_launches(const fftc_plan* plan);
  * given by fftc_plan_split().                                              */
 int fftc_factorize(int64_t N, int* radices, int max);
 
+/* Planner introspection (host only): names of the compiled single-pass
+ * schedules for N, default first; writes up to `max` pointers to static
+ * strings, returns the count.  Setting the environment variable
+ * FFTC_KERNEL=<name> before fftc_plan_create pins the planner to that
+ * candidate (used by the tuner, tools/tune.py, and the per-candidate tests). */
+int fftc_candidates(int64_t N, const char** names, int max);
+
 /* Top-level split used for N: returns 1 (single pass: *M = N, *K = 1),
  * 2 (four-step: N = M*K, column DFT_M then row DFT_K), or -1 unsupported. */
 int fftc_plan_split(int64_t N, int64_t* M, int64_t* K);

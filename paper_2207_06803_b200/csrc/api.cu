@@ -326,6 +326,16 @@ int fftc_plan_describe(const fftc_plan* p, char* buf, size_t len) {
   return n;
 }
 
+int fftc_candidates(int64_t N, const char** names, int max) {
+  int c = 0;
+  for (int i = 0; i < fused_count(); ++i)
+    if (fused_at(i)->N == N) {
+      if (names && c < max) names[c] = fused_at(i)->name;
+      ++c;
+    }
+  return c;
+}
+
 int fftc_factorize(int64_t N, int* radices, int max) { return single_pass_radices(N, radices, max); }
 
 int fftc_plan_split(int64_t N, int64_t* M, int64_t* K) { return top_split(N, M, K); }

@@ -24,6 +24,7 @@
 //            f*(N|1) + i (odd stride -> conflict free across transforms).
 #pragma once
 #include "codelets.cuh"
+#include "tma.cuh"
 
 namespace fftc {
 
@@ -368,6 +369,100 @@ static cudaError_t launch_fused_batch(const float2* in, float2* out, const float
   if (grid == 0) return cudaSuccess;
   if (grid > 0x7fffffffLL) return cudaErrorInvalidValue;
   kern<<<(unsigned)grid, P::THREADS, P::SMEM, st>>>(in, out, tw, batch, conj ? -1.0f : 1.0f);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- persistent TMA-fed kernel
+// LT_FAST schedules (S >= 2).  Each CTA loops over tiles of FPB contiguous transforms.
+// A tile is brought HBM -> shared by one bulk asynchronous copy (cp.async.bulk, TMA
+// engine, completion on an mbarrier) into a linear buffer LIN; stage 0 reads LIN and
+// writes the swizzled exchange buffer WORK; as soon as every thread has read LIN, the
+// copy of the CTA's next tile is issued, so it streams in while stages 1..S-1 run and
+// the last stage stores HBM directly.
+template <class P, int MINB>
+__global__ void __launch_bounds__(P::THREADS, MINB)
+    k_fused_tma(const float2* __restrict__ in, float2* __restrict__ out, const float2* __restrict__ tw,
+                long long batch, float csign) {
+  static_assert(P::MAP == LT_FAST && P::S >= 2, "TMA kernel: LT_FAST, at least two stages");
+  constexpr int N = P::N, FPB = P::FPB;
+  constexpr int WORK = ((P::SS * FPB) + 1) & ~1;  // keep LIN 16-byte aligned
+  extern __shared__ __align__(128) float2 sm[];
+  float2* work = sm;
+  float2* lin = sm + WORK;
+  __shared__ __align__(8) uint64_t bar;
+  int f, lt;
+  P::thread_coords(threadIdx.x, f, lt);
+  const long long ntiles = (batch + FPB - 1) / FPB;
+  auto tile_nf = [&](long long t) {
+    const long long rem = batch - t * FPB;
+    return rem < FPB ? (int)rem : FPB;
+  };
+  auto tile_tma = [&](long long t) { return ((long long)tile_nf(t) * N * 8) % 16 == 0; };
+  auto issue = [&](long long t) {
+    const uint32_t bytes = (uint32_t)tile_nf(t) * N * 8u;
+    mbar_arrive_expect_tx(&bar, bytes);
+    bulk_g2s(lin, in + t * FPB * (long long)N, bytes, &bar);
+  };
+  if (threadIdx.x == 0) mbar_init(&bar, 1);
+  __syncthreads();
+  long long t = blockIdx.x;
+  uint32_t phase = 0;
+  if (threadIdx.x == 0 && t < ntiles && tile_tma(t)) issue(t);
+  for (; t < ntiles; t += gridDim.x) {
+    const int nf = tile_nf(t);
+    const bool fvalid = f < nf;
+    if (tile_tma(t)) {
+      mbar_wait(&bar, phase);
+      phase ^= 1;
+    } else {  // ragged odd-length tail tile: plain copy
+      const float2* g = in + t * FPB * (long long)N;
+      for (int e = threadIdx.x; e < nf * N; e += P::THREADS) lin[e] = g[e];
+    }
+    __syncthreads();  // WORK free (previous tile's last stage done), LIN visible
+    float2* go = out + t * FPB * (long long)N + (long long)f * N;
+    const float2* gl = lin + f * N;
+    auto gstore = [&](int i, float2 v) { __stcs(go + i, make_float2(v.x, csign * v.y)); };
+    stage<P, 0, true, false>(
+        work, f, lt, fvalid, tw,
+        [&](int i) {
+          const float2 a = gl[i];
+          return make_float2(a.x, csign * a.y);
+        },
+        gstore);
+    fence_proxy_async_smem();
+    __syncthreads();  // every thread has read LIN
+    if (threadIdx.x == 0) {
+      const long long tn = t + gridDim.x;
+      if (tn < ntiles && tile_tma(tn)) issue(tn);
+    }
+    sfor<P::S - 1>([&](auto s_) {
+      constexpr int s = decltype(s_)::value + 1;
+      stage<P, s, false, s == P::S - 1>(work, f, lt, fvalid, tw, [&](int) { return make_float2(0.f, 0.f); },
+                                        gstore);
+    });
+  }
+}
+
+template <class P, int MINB>
+static cudaError_t launch_fused_tma(const float2* in, float2* out, const float2* tw, long long batch, int conj,
+                                    cudaStream_t st) {
+  auto kern = k_fused_tma<P, MINB>;
+  constexpr size_t smem = (size_t)((((P::SS * P::FPB) + 1) & ~1) + P::N * P::FPB) * sizeof(float2);
+  static int grid_max = 0;
+  if (!grid_max) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, P::THREADS, smem);
+    if (e != cudaSuccess) return e;
+    grid_max = sms * (per > 0 ? per : 1);
+  }
+  const long long ntiles = (batch + P::FPB - 1) / P::FPB;
+  if (ntiles == 0) return cudaSuccess;
+  const unsigned grid = (unsigned)(ntiles < grid_max ? ntiles : grid_max);
+  kern<<<grid, P::THREADS, smem, st>>>(in, out, tw, batch, conj ? -1.0f : 1.0f);
   return cudaGetLastError();
 }
 

@@ -1,0 +1,28 @@
+// kernels_large.cu -- compiled single-pass schedules, large sizes (product path).
+// Row: name, N, radix list (R_0 = leaf DFT, innermost level of Eq. 2), threads per
+// transform, transforms per CTA, mapping, direct HBM I/O, min CTAs/SM, radices.  The first
+// row for an N is the planner's default; the others are candidates (tools/tune.py).
+#include "kernels_common.cuh"
+
+namespace fftc {
+
+extern const FusedEntry kTable_large[];
+extern const int kCount_large;
+const FusedEntry kTable_large[] = {
+    FFTC_ENTRY("n2048_r16x16x8_t128x1", 2048, Rad_16x16x8, 128, 1, LT_FAST, true, 6, 16, 16, 8),
+    FFTC_ENTRY("n2048_r8x16x16_t128x2", 2048, Rad_8x16x16, 128, 2, LT_FAST, true, 3, 8, 16, 16),
+    FFTC_ENTRY("n2048_r16x16x8_t128x2", 2048, Rad_16x16x8, 128, 2, LT_FAST, true, 3, 16, 16, 8),
+    FFTC_TMA("n2048_r8x16x16_t128x1_tma", 2048, Rad_8x16x16, 128, 1, 6, 8, 16, 16),
+    FFTC_ENTRY("n4096_r16x16x16_t128x1", 4096, Rad_16x16x16, 128, 1, LT_FAST, true, 4, 16, 16, 16),
+    FFTC_ENTRY("n4096_r16x16x16_t256x1", 4096, Rad_16x16x16, 256, 1, LT_FAST, true, 3, 16, 16, 16),
+    FFTC_TMA("n4096_r16x16x16_t256x1_tma", 4096, Rad_16x16x16, 256, 1, 3, 16, 16, 16),
+    FFTC_ENTRY("n2048_r16x16x8_t256x1", 2048, Rad_16x16x8, 256, 1, LT_FAST, true, 4, 16, 16, 8),
+    FFTC_ENTRY("n2048_r16x8x16_t128x1", 2048, Rad_16x8x16, 128, 1, LT_FAST, true, 6, 16, 8, 16),
+    FFTC_ENTRY("n4096_r16x16x16_t128x1m6", 4096, Rad_16x16x16, 128, 1, LT_FAST, true, 5, 16, 16, 16),
+    FFTC_ENTRY("n4096_r16x32x8_t256x1", 4096, Rad_16x32x8, 256, 1, LT_FAST, true, 3, 16, 32, 8),
+    FFTC_ENTRY("n4096_r8x32x16_t256x1", 4096, Rad_8x32x16, 256, 1, LT_FAST, true, 3, 8, 32, 16),
+    FFTC_ENTRY("n4096_r8x8x8x8_t512x1", 4096, Rad_8x8x8x8, 512, 1, LT_FAST, true, 2, 8, 8, 8, 8),
+};
+const int kCount_large = (int)(sizeof(kTable_large) / sizeof(kTable_large[0]));
+
+}  // namespace fftc

@@ -48,7 +48,7 @@ def smooth7(n):
     return n == 1
 
 
-ALLOWED = {2, 3, 4, 5, 7, 8, 9, 10, 14, 15, 16, 25, 27, 32}
+ALLOWED = {2, 3, 4, 5, 7, 8, 9, 10, 14, 15, 16, 25, 27, 30, 32}
 
 
 @pytest.mark.parametrize("N", [n for n in range(1, 4097) if smooth7(n)])
@@ -72,8 +72,10 @@ def test_planner_bench_sizes():
     # SURVEY §8(a) a1 examples (compiled schedules)
     assert fftc.fftc_factorize(4096) == [16, 16, 16]
     assert fftc.fftc_factorize(64) == [8, 8]
-    assert fftc.fftc_factorize(60) == [4, 3, 5]
-    assert fftc.fftc_factorize(105) == [3, 5, 7]
+    assert fftc.fftc_factorize(60) == [4, 15]
+    assert fftc.fftc_factorize(105) == [7, 15]
+    for N in (8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096, 60, 105, 210, 1000, 2187, 3125):
+        assert fftc.fftc_candidates(N), N  # a compiled fast schedule exists for every BASELINE size
     assert math.prod(fftc.fftc_factorize(2187)) == 2187
     assert math.prod(fftc.fftc_factorize(3125)) == 3125
 

@@ -99,6 +99,6 @@ def test_config5_loopback_2p30():
     torch.cuda.synchronize()
     pi.close()
     del y
-    num = torch.linalg.vector_norm((z / N - d).double())
-    den = torch.linalg.vector_norm(d.double())
+    num = torch.linalg.vector_norm(torch.view_as_real(z / N - d).double())
+    den = torch.linalg.vector_norm(torch.view_as_real(d).double())
     assert (num / den).item() <= 2 * oracle.tolerance(N)

@@ -80,6 +80,22 @@ def test_fourstep_small_batch(N, sign):
     check(y, x, sign)
 
 
+@pytest.mark.parametrize("N", POW2 + MIXED)
+def test_every_candidate_schedule(N, monkeypatch):
+    """Every compiled schedule (not just the planner's default) is correct, both signs, ragged batch."""
+    names = fftc.fftc_candidates(N)
+    assert names
+    x = synth.uniform_c64(N, 37, seed=N)
+    for name in names:
+        monkeypatch.setenv("FFTC_KERNEL", name)
+        for sign in (-1, 1):
+            with fftc.Plan(N, 37, sign) as p:
+                assert name in p.describe()
+                y = p(torch.from_numpy(x).cuda())
+            torch.cuda.synchronize()
+            check(y.cpu().numpy(), x, sign)
+
+
 # ---------------------------------------------------------------- full BASELINE sizes (sampled)
 @pytest.mark.parametrize("N", POW2)
 @pytest.mark.parametrize("sign", [-1, 1])
