@@ -312,8 +312,8 @@ int fftc_plan_describe(const fftc_plan* p, char* buf, size_t len) {
       rad(p->ce->R, p->ce->S);
       n += snprintf(tmp + n, sizeof(tmp) - n, " rows=");
       rad(p->re->R, p->re->S);
-      n += snprintf(tmp + n, sizeof(tmp) - n, " workspace=%lld launches=2",
-                    (long long)(p->N * p->batch * (int64_t)sizeof(float2)));
+      n += snprintf(tmp + n, sizeof(tmp) - n, " col_kernel=%s row_kernel=%s workspace=%lld launches=2", p->ce->name,
+                    p->re->name, (long long)(p->N * p->batch * (int64_t)sizeof(float2)));
       break;
     case KIND_DIST:
       n += dist_describe(p->dist, tmp + n, sizeof(tmp) - n);

@@ -22,6 +22,12 @@
 namespace fftc {
 
 
+// w_T^e for 0 <= e < T from the two-level tables A[e mod 4096] * B[e div 4096]
+__device__ __forceinline__ float2 root_lookup(const float2* __restrict__ A, const float2* __restrict__ B,
+                                              long long e) {
+  return cmul(__ldg(A + (e & 4095)), __ldg(B + (e >> 12)));
+}
+
 template <class P, bool OUT_T, int MINB>
 __global__ void __launch_bounds__(P::THREADS, MINB)
     k_colx(const float2* __restrict__ in, float2* __restrict__ out, const float2* __restrict__ tw,
@@ -31,6 +37,9 @@ __global__ void __launch_bounds__(P::THREADS, MINB)
   static_assert(P::MAP == F_FAST, "column kernel walks columns");
   constexpr int L = P::N;
   constexpr int C = P::FPB;
+  constexpr int RL = P::R(P::S - 1);   // last-stage radix
+  constexpr int NSL = P::ns(P::S - 1); // last-stage Ns: outputs k = j + r NSL
+  constexpr int NB2 = ilog2(highbit(RL - 1)) + 1;  // powers w^(2^b) needed for r < RL
   int f, lt;
   P::thread_coords(threadIdx.x, f, lt);
   const long long grp = blockIdx.x / g.tiles;
@@ -38,10 +47,28 @@ __global__ void __launch_bounds__(P::THREADS, MINB)
   const int ci = ci0 + f;
   const float2* gi = in + grp * g.in_g + ci;
   const long long omask = (1LL << g.ocl) - 1;
-  auto twiddle = [&](int cc, int k, float2 v) {
+  // Output twiddle w_T^{c k}, c = (ci >> tw_shift) + tw_off.  In the last stage a thread's
+  // outputs are k = j + r NSL: w^{c k} = w^{c j} (w^{c NSL})^r -- one table lookup per
+  // butterfly for the base, the step powers w^{c NSL 2^b} once per thread, and at most
+  // popcount(r) complex products per element (all from tables built in double).
+  const long long ctw = g.tw ? (long long)(ci >> g.tw_shift) + g.tw_off : 0;
+  float2 sp[NB2];
+  if (g.tw) {
+    sp[0] = root_lookup(twA, twB, ctw * NSL);
+    sfor<NB2 - 1>([&](auto b_) {
+      constexpr int b = decltype(b_)::value + 1;
+      sp[b] = cmul(sp[b - 1], sp[b - 1]);
+    });
+  }
+  float2 base = make_float2(1.f, 0.f);
+  auto twiddle = [&](int k, float2 v, int r) {
     if (g.tw) {
-      const long long e = ((long long)(cc >> g.tw_shift) + g.tw_off) * k;
-      const float2 w = cmul(__ldg(twA + (e & 4095)), __ldg(twB + (e >> 12)));
+      if (r == 0) base = root_lookup(twA, twB, ctw * k);
+      float2 w = base;
+      sfor<NB2>([&](auto b_) {
+        constexpr int b = decltype(b_)::value;
+        if (r & (1 << b)) w = cmul(w, sp[b]);
+      });
       v = cmul(v, w);
     }
     return v;
@@ -52,13 +79,15 @@ __global__ void __launch_bounds__(P::THREADS, MINB)
   };
   if constexpr (!OUT_T) {
     float2* go = out + grp * g.out_g + ci * g.out_c;
-    run_stages<P, true, true>(sm, f, lt, true, tw, load, [&](int k, float2 v) {
-      v = twiddle(ci, k, v);
+    run_stages<P, true, true>(sm, f, lt, true, tw, load, [&](int k, float2 v, int r) {
+      v = twiddle(k, v, r);
       __stcs(go + ((long long)k >> g.ocl) * g.out_cs + ((long long)k & omask) * g.out_s,
              make_float2(v.x, csign_out * v.y));
     });
   } else {
-    run_stages<P, true, false>(sm, f, lt, true, tw, load, [&](int, float2) {});
+    // last stage: twiddled values back into the exchange buffer, then a store walking k
+    run_stages<P, true, true, true>(sm, f, lt, true, tw, load,
+                                    [&](int k, float2 v, int r) { sm[P::sidx(f, k)] = twiddle(k, v, r); });
     __syncthreads();
     float2* go = out + grp * g.out_g;
     constexpr int TOTAL = L * C;
@@ -68,7 +97,7 @@ __global__ void __launch_bounds__(P::THREADS, MINB)
       constexpr int n = decltype(n_)::value;
       const int e = threadIdx.x + n * P::THREADS;
       const int k = e % L, cc = e / L;
-      float2 v = twiddle(ci0 + cc, k, sm[P::sidx(cc, k)]);
+      const float2 v = sm[P::sidx(cc, k)];
       __stcs(go + (long long)(ci0 + cc) * g.out_c + ((long long)k >> g.ocl) * g.out_cs +
                  ((long long)k & omask) * g.out_s,
              make_float2(v.x, csign_out * v.y));

@@ -12,6 +12,9 @@
 // crosses HBM twice (read+write per pass): 32 B per complex element.
 // The D^N_M twiddle w_N^e, e = r j < N, is read as A[e mod 4096] * B[e div 4096]
 // (two fp32 tables built in double on the host, both L1/L2 resident).
+#include <stdlib.h>
+#include <string.h>
+
 #include "colfft.cuh"
 #include "fourstep.h"
 
@@ -34,7 +37,7 @@ __global__ void __launch_bounds__(P::THREADS, MINB)
   const int j0 = (blockIdx.x % tiles) * FPB;
   const float2* gi = work + b * N + (long long)(j0 + f) * K;
   run_stages<P, true, false>(
-      sm, f, lt, true, tw, [&](int i) { return __ldcs(gi + i); }, [&](int, float2) {});
+      sm, f, lt, true, tw, [&](int i) { return __ldcs(gi + i); }, [&](int, float2, int) {});
   __syncthreads();  // the transposed store reads rows written by other warps
   // X[j + M k1] for j in [j0, j0 + FPB): FPB contiguous outputs per k1; lanes walk j
   // (row stride SS chosen so a 16-lane phase hits 16 banks), 8-byte stores.
@@ -70,39 +73,68 @@ cudaError_t launch_rows(const float2* work, float2* out, const float2* tw, int M
 
 }  // namespace
 
-#define FFTC_COL(M, RAD, TPF, C, LAY, MINB, ...)                                                  \
+#define FFTC_COL(NAME, M, RAD, TPF, C, LAY, MINB, ...)                                            \
   {M, RAD::S, {__VA_ARGS__}, TPF, C, Sched<M, RAD, TPF, C, F_FAST, 0, LAY>::SMEM,                 \
    Sched<M, RAD, TPF, C, F_FAST, 0, LAY_ODD>::SMEM, &launch_colx<Sched<M, RAD, TPF, C, F_FAST, 0, LAY>, false, MINB>, \
-   &launch_colx<Sched<M, RAD, TPF, C, F_FAST, 0, LAY_ODD>, true, MINB>}
-#define FFTC_ROW(K, RAD, TPF, FPB, PAD, MINB, ...)                                           \
+   &launch_colx<Sched<M, RAD, TPF, C, F_FAST, 0, LAY_ODD>, true, MINB>, NAME}
+#define FFTC_ROW(NAME, K, RAD, TPF, FPB, PAD, MINB, ...)                                     \
   {K, RAD::S, {__VA_ARGS__}, TPF, FPB, Sched<K, RAD, TPF, FPB, LT_FAST, PAD>::SMEM,         \
-   &launch_rows<Sched<K, RAD, TPF, FPB, LT_FAST, PAD>, MINB>}
+   &launch_rows<Sched<K, RAD, TPF, FPB, LT_FAST, PAD>, MINB>, NAME}
 
 using Rad_16x16 = Radices<16, 16>;
 using Rad_16x32 = Radices<16, 32>;
+using Rad_32x16 = Radices<32, 16>;
 using Rad_8x16x16 = Radices<8, 16, 16>;
+using Rad_16x16x8 = Radices<16, 16, 8>;
+using Rad_16x16x4 = Radices<16, 16, 4>;
 using Rad_16x16x16 = Radices<16, 16, 16>;
 using Rad_32x32 = Radices<32, 32>;
 
+// First entry per length = default; others are tuning candidates (FFTC_COL / FFTC_ROW = name).
 static const ColEntry kCols[] = {
-    FFTC_COL(256, Rad_16x16, 16, 16, LAY_FXOR, 2, 16, 16),
-    FFTC_COL(512, Rad_16x32, 16, 16, LAY_FXOR, 1, 16, 32),
-    FFTC_COL(1024, Rad_32x32, 32, 8, LAY_INTER, 1, 32, 32),
-    FFTC_COL(2048, Rad_8x16x16, 128, 4, LAY_INTER, 1, 8, 16, 16),
-    FFTC_COL(4096, Rad_16x16x16, 256, 4, LAY_INTER, 1, 16, 16, 16),
+    FFTC_COL("c256_r16x16_t16x16", 256, Rad_16x16, 16, 16, LAY_FXOR, 2, 16, 16),
+    FFTC_COL("c256_r16x16_t16x32", 256, Rad_16x16, 16, 32, LAY_FXOR, 1, 16, 16),
+    FFTC_COL("c256_r16x16_t16x8", 256, Rad_16x16, 16, 8, LAY_INTER, 4, 16, 16),
+    FFTC_COL("c512_r16x32_t16x16", 512, Rad_16x32, 16, 16, LAY_FXOR, 1, 16, 32),
+    FFTC_COL("c512_r32x16_t16x16", 512, Rad_32x16, 16, 16, LAY_FXOR, 1, 32, 16),
+    FFTC_COL("c512_r32x16_t16x8", 512, Rad_32x16, 16, 8, LAY_INTER, 2, 32, 16),
+    FFTC_COL("c1024_r32x32_t32x8", 1024, Rad_32x32, 32, 8, LAY_INTER, 1, 32, 32),
+    FFTC_COL("c1024_r32x32_t32x4", 1024, Rad_32x32, 32, 4, LAY_INTER, 2, 32, 32),
+    FFTC_COL("c1024_r32x32_t32x16", 1024, Rad_32x32, 32, 16, LAY_FXOR, 1, 32, 32),
+    FFTC_COL("c1024_r16x16x4_t64x8", 1024, Rad_16x16x4, 64, 8, LAY_INTER, 1, 16, 16, 4),
+    FFTC_COL("c2048_r8x16x16_t128x4", 2048, Rad_8x16x16, 128, 4, LAY_INTER, 1, 8, 16, 16),
+    FFTC_COL("c2048_r16x16x8_t128x4", 2048, Rad_16x16x8, 128, 4, LAY_INTER, 1, 16, 16, 8),
+    FFTC_COL("c2048_r16x16x8_t128x2", 2048, Rad_16x16x8, 128, 2, LAY_INTER, 2, 16, 16, 8),
+    FFTC_COL("c4096_r16x16x16_t256x4", 4096, Rad_16x16x16, 256, 4, LAY_INTER, 1, 16, 16, 16),
+    FFTC_COL("c4096_r16x16x16_t256x2", 4096, Rad_16x16x16, 256, 2, LAY_INTER, 2, 16, 16, 16),
+    FFTC_COL("c4096_r16x16x16_t128x4", 4096, Rad_16x16x16, 128, 4, LAY_INTER, 1, 16, 16, 16),
 };
 static const RowEntry kRows[] = {
-    FFTC_ROW(256, Rad_16x16, 16, 32, 1, 1, 16, 16),
-    FFTC_ROW(1024, Rad_32x32, 32, 8, 2, 1, 32, 32),
-    FFTC_ROW(4096, Rad_16x16x16, 256, 4, 4, 1, 16, 16, 16),
+    FFTC_ROW("r256_r16x16_t16x32", 256, Rad_16x16, 16, 32, 1, 1, 16, 16),
+    FFTC_ROW("r256_r16x16_t16x16", 256, Rad_16x16, 16, 16, 1, 2, 16, 16),
+    FFTC_ROW("r256_r16x16_t16x8", 256, Rad_16x16, 16, 8, 2, 4, 16, 16),
+    FFTC_ROW("r512_r32x16_t16x16", 512, Rad_32x16, 16, 16, 1, 2, 32, 16),
+    FFTC_ROW("r1024_r32x32_t32x8", 1024, Rad_32x32, 32, 8, 2, 1, 32, 32),
+    FFTC_ROW("r1024_r32x32_t32x4", 1024, Rad_32x32, 32, 4, 4, 2, 32, 32),
+    FFTC_ROW("r1024_r32x32_t32x16", 1024, Rad_32x32, 32, 16, 1, 1, 32, 32),
+    FFTC_ROW("r2048_r16x16x8_t128x4", 2048, Rad_16x16x8, 128, 4, 4, 2, 16, 16, 8),
+    FFTC_ROW("r4096_r16x16x16_t256x4", 4096, Rad_16x16x16, 256, 4, 4, 1, 16, 16, 16),
+    FFTC_ROW("r4096_r16x16x16_t256x2", 4096, Rad_16x16x16, 256, 2, 8, 2, 16, 16, 16),
+    FFTC_ROW("r4096_r16x16x16_t128x4", 4096, Rad_16x16x16, 128, 4, 4, 2, 16, 16, 16),
 };
 
 const ColEntry* find_col(int M) {
+  if (const char* want = getenv("FFTC_COL"))
+    for (const auto& e : kCols)
+      if (e.M == M && strcmp(e.name, want) == 0) return &e;
   for (const auto& e : kCols)
     if (e.M == M) return &e;
   return nullptr;
 }
 const RowEntry* find_row(int K) {
+  if (const char* want = getenv("FFTC_ROW"))
+    for (const auto& e : kRows)
+      if (e.K == K && strcmp(e.name, want) == 0) return &e;
   for (const auto& e : kRows)
     if (e.K == K) return &e;
   return nullptr;

@@ -23,6 +23,7 @@ struct ColEntry {
   size_t smem, smem_t;
   colx_launch_fn launch;
   colx_launch_fn launch_t;
+  const char* name;
 };
 // DFT_K along FPB rows per CTA + transposed store X[j + M k1] (four-step pass 2).
 struct RowEntry {
@@ -32,6 +33,7 @@ struct RowEntry {
   int tpf, rows;
   size_t smem;
   row_launch_fn launch;
+  const char* name;
 };
 
 const ColEntry* find_col(int M);

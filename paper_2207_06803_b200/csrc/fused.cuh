@@ -113,11 +113,13 @@ struct Sched {
   }
 };
 
-// One Stockham stage.  SRC_G: stage reads HBM through gload(i) (else shared);
-// DST_G: stage writes HBM through gstore(i, v) (else shared).
+// One Stockham stage.  SRC_G: stage reads through gload(i) (HBM, or a staging
+// buffer); DST_G: stage writes through gstore(i, v, r) (HBM, or shared memory in
+// the transposed-output column kernel: then MID_SYNC forces the in-place barrier
+// between the reads and the writes); r = the element's index within its butterfly.
 // Twiddle table layout (per plan, built on the host in double): stage s occupies
 // entries [Ns-1, Ns-1 + (R-1) Ns), entry (Ns-1) + (r-1) Ns + m = w_L^{m r}.
-template <class P, int s, bool SRC_G, bool DST_G, class GL, class GS>
+template <class P, int s, bool SRC_G, bool DST_G, bool MID_SYNC = false, class GL, class GS>
 __device__ __forceinline__ void stage(float2* sm, int f, int lt, bool fvalid,
                                       const float2* __restrict__ tw, GL&& gload, GS&& gstore) {
   constexpr int R = P::R(s);
@@ -139,7 +141,7 @@ __device__ __forceinline__ void stage(float2* sm, int f, int lt, bool fvalid,
       });
     }
   });
-  if constexpr (!SRC_G && !DST_G) P::sync();
+  if constexpr ((!SRC_G && !DST_G) || MID_SYNC) P::sync();
   sfor<KB>([&](auto k_) {
     constexpr int k = decltype(k_)::value;
     const int j = lt + k * P::TPF;
@@ -162,7 +164,7 @@ __device__ __forceinline__ void stage(float2* sm, int f, int lt, bool fvalid,
       const int o = (Ns == 1) ? j * R : ((j / Ns) * L + m);
       sfor<R>([&](auto r_) {
         constexpr int r = decltype(r_)::value;
-        if constexpr (DST_G) gstore(o + r * Ns, v[k][r]);
+        if constexpr (DST_G) gstore(o + r * Ns, v[k][r], r);
         else sm[P::sidx(f, o + r * Ns)] = v[k][r];
       });
     }
@@ -170,13 +172,15 @@ __device__ __forceinline__ void stage(float2* sm, int f, int lt, bool fvalid,
   if constexpr (!DST_G) P::sync();
 }
 
-// All S stages.  SRC0_G: stage 0 reads HBM; DSTL_G: the last stage writes HBM.
-template <class P, bool SRC0_G, bool DSTL_G, class GL, class GS>
+// All S stages.  SRC0_G: stage 0 reads HBM; DSTL_G: the last stage writes through
+// gstore; LAST_MID: the last stage's gstore writes the shared exchange buffer.
+template <class P, bool SRC0_G, bool DSTL_G, bool LAST_MID = false, class GL, class GS>
 __device__ __forceinline__ void run_stages(float2* sm, int f, int lt, bool fvalid,
                                            const float2* __restrict__ tw, GL&& gload, GS&& gstore) {
   sfor<P::S>([&](auto s_) {
     constexpr int s = decltype(s_)::value;
-    stage<P, s, SRC0_G && s == 0, DSTL_G && s == P::S - 1>(sm, f, lt, fvalid, tw, gload, gstore);
+    stage<P, s, SRC0_G && s == 0, DSTL_G && s == P::S - 1, LAST_MID && s == P::S - 1>(sm, f, lt, fvalid, tw, gload,
+                                                                                        gstore);
   });
 }
 
@@ -343,12 +347,12 @@ __global__ void __launch_bounds__(P::THREADS, MINB)
           float2 a = __ldcs(gi + i);
           return make_float2(a.x, csign * a.y);
         },
-        [&](int i, float2 v) { __stcs(go + i, make_float2(v.x, csign * v.y)); });
+        [&](int i, float2 v, int) { __stcs(go + i, make_float2(v.x, csign * v.y)); });
   } else {
     tile_in<P>(sm, gin, nf, csign);
     __syncthreads();
     run_stages<P, false, false>(
-        sm, f, lt, fvalid, tw, [&](int) { return make_float2(0.f, 0.f); }, [&](int, float2) {});
+        sm, f, lt, fvalid, tw, [&](int) { return make_float2(0.f, 0.f); }, [&](int, float2, int) {});
     __syncthreads();
     tile_out<P>(sm, gout, nf, 1.0f * csign);
   }
@@ -421,7 +425,7 @@ __global__ void __launch_bounds__(P::THREADS, MINB)
     __syncthreads();  // WORK free (previous tile's last stage done), LIN visible
     float2* go = out + t * FPB * (long long)N + (long long)f * N;
     const float2* gl = lin + f * N;
-    auto gstore = [&](int i, float2 v) { __stcs(go + i, make_float2(v.x, csign * v.y)); };
+    auto gstore = [&](int i, float2 v, int) { __stcs(go + i, make_float2(v.x, csign * v.y)); };
     stage<P, 0, true, false>(
         work, f, lt, fvalid, tw,
         [&](int i) {

@@ -10,6 +10,8 @@
 // balanced pair with compiled column (DFT_M) and row (DFT_K) pass kernels.
 #include "planner.h"
 
+#include <stdlib.h>
+
 #include "fourstep.h"
 #include "registry.h"
 
@@ -71,9 +73,11 @@ int top_split(int64_t N, int64_t* M, int64_t* K) {
     return 1;
   }
   int64_t bestM = 0, bestK = 0;
+  const char* force = getenv("FFTC_SPLIT_M");  // tuning: pin the top-level split
   for (int i = 0; i < col_count(); ++i) {
     const ColEntry* c = col_at(i);
     if (N % c->M) continue;
+    if (force && atoll(force) != c->M) continue;
     const int64_t k = N / c->M;
     if (k > 0x7fffffff || !find_row((int)k)) continue;
     const int64_t d = (c->M > k) ? c->M - k : k - c->M;
