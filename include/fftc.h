@@ -101,9 +101,17 @@ int fftc_factorize(int64_t N, int* radices, int max);
  * candidate (used by the tuner, tools/tune.py, and the per-candidate tests). */
 int fftc_candidates(int64_t N, const char** names, int max);
 
-/* Top-level split used for N: returns 1 (single pass: *M = N, *K = 1),
- * 2 (four-step: N = M*K, column DFT_M then row DFT_K), or -1 unsupported. */
+/* Two-level split for N: returns 1 (single pass: *M = N, *K = 1),
+ * 2 (four-step: N = M*K, column DFT_M then row DFT_K), or -1 unsupported.
+ * Powers of two above 4096 run the multi-pass path instead (fftc_plan_passes)
+ * unless FFTC_LARGE=fourstep is set.                                       */
 int fftc_plan_split(int64_t N, int64_t* M, int64_t* K);
+
+/* Multi-pass split (host only): power-of-two N in [2^9, 2^48] as
+ * p = ceil(log2 N / 8) passes of lengths L_s in [16, 256], product N,
+ * each one level of Eq. 2 in Stockham form over HBM.  Writes up to `max`
+ * lengths, returns p, or -1 if N is not such a power of two.              */
+int fftc_plan_passes(int64_t N, int* lengths, int max);
 
 /* ---------------------------------------------------------------------
  * Distributed six-step (one process per GPU, NCCL over NVLink/NVSwitch).

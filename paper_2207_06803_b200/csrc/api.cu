@@ -7,6 +7,7 @@
 // and codelet is the forward w_N = exp(-2 pi i / N) of PAPER.md P:46.
 #include <math.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <vector>
@@ -77,6 +78,8 @@ cudaError_t exec_local(const fftc_plan* p, const float2* in, float2* out, long l
       return p->fe->launch(in, out, p->d_tw, batch, conj, st);
     case KIND_GENERIC:
       return launch_generic(p->gs, in, out, p->d_tw, batch, conj, st);
+    case KIND_PASSES:
+      return passes_execute(p->pp, in, out, work, batch, conj, st);
     case KIND_FOURSTEP: {
       const ColGeom g = fourstep_cols_geom(p->ce, p->N, p->K);
       cudaError_t e = p->ce->launch(in, work, p->d_tw, p->d_twA, p->d_twB, g, batch, conj, 0, st);
@@ -105,6 +108,11 @@ static void free_plan(fftc_plan* p) {
   cudaFree(p->d_twA);
   cudaFree(p->d_twB);
   cudaFree(p->d_work);
+  for (int s = 0; s < kMaxPasses; ++s) {
+    cudaFree(p->pp.tw[s]);
+    cudaFree(p->pp.twA[s]);
+    cudaFree(p->pp.twB[s]);
+  }
   if (p->hs) {
     for (int i = 0; i < HostStage::kDepth; ++i) {
       cudaFree(p->hs->d_in[i]);
@@ -157,7 +165,6 @@ fftc_plan* fftc_plan_create(int64_t N, int64_t batch, int sign) {
   }
   int64_t M = 0, K = 0;
   const int split = top_split(N, &M, &K);
-  if (split < 0) return fail(p, FFTC_ERROR_UNSUPPORTED_SIZE);
   if (split == 1) {
     int R[kMaxStages];
     const FusedEntry* fe = find_fused((int)N);
@@ -177,7 +184,36 @@ fftc_plan* fftc_plan_create(int64_t N, int64_t batch, int sign) {
     if (err != cudaSuccess) return fail(p, from_cuda(err));
     return p;
   }
+  // multi-pass TMA path for powers of two (FFTC_LARGE=fourstep selects the two-pass kernels)
+  int Ls[kMaxPasses];
+  const char* large = getenv("FFTC_LARGE");
+  const int np = pass_split(N, Ls, kMaxPasses);
+  // measured on B200: two TMA passes beat the four-step at 2^16; at 2^17..2^23 the
+  // four-step's two passes beat three TMA passes; from 2^24 the TMA passes win
+  bool use_passes = np > 0 && passes_available() && (np == 2 || split < 0 || N >= ((int64_t)1 << 24));
+  if (large && strcmp(large, "fourstep") == 0) use_passes = false;
+  if (large && strcmp(large, "passes") == 0 && np > 0 && passes_available()) use_passes = true;
+  if (use_passes) {
+    p->kind = KIND_PASSES;
+    p->pp.N = N;
+    p->pp.p = np;
+    int64_t Ns = 1;
+    for (int s = 0; s < np && err == cudaSuccess; ++s) {
+      const PassEntry* e = find_pass(Ls[s]);
+      if (!e) return fail(p, FFTC_ERROR_UNSUPPORTED_SIZE);
+      p->pp.e[s] = e;
+      const int64_t T = Ns * Ls[s];
+      p->pp.tw[s] = upload_stage_table(Ls[s], e->R, e->S, &err);
+      if (err == cudaSuccess) p->pp.twA[s] = upload_root_table(T, T < 4096 ? T : 4096, 1, &err);
+      if (err == cudaSuccess) p->pp.twB[s] = upload_root_table(T, (T + 4095) / 4096, 4096, &err);
+      Ns = T;
+    }
+    if (err == cudaSuccess && batch > 0 && np > 1) err = cudaMalloc(&p->d_work, (size_t)(N * batch) * sizeof(float2));
+    if (err != cudaSuccess) return fail(p, from_cuda(err));
+    return p;
+  }
   // four-step
+  if (split < 0) return fail(p, FFTC_ERROR_UNSUPPORTED_SIZE);
   p->kind = KIND_FOURSTEP;
   p->M = M;
   p->K = K;
@@ -228,7 +264,8 @@ fftc_status fftc_execute_host(fftc_plan* p, const void* host_in, void* host_out)
     for (int i = 0; i < HostStage::kDepth && e == cudaSuccess; ++i) {
       e = cudaMalloc(&hs->d_in[i], (size_t)(chunk * tbytes));
       if (e == cudaSuccess) e = cudaMalloc(&hs->d_out[i], (size_t)(chunk * tbytes));
-      if (e == cudaSuccess && p->kind == KIND_FOURSTEP) e = cudaMalloc(&hs->d_work[i], (size_t)(chunk * tbytes));
+      if (e == cudaSuccess && (p->kind == KIND_FOURSTEP || p->kind == KIND_PASSES))
+        e = cudaMalloc(&hs->d_work[i], (size_t)(chunk * tbytes));
       if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&hs->st[i], cudaStreamNonBlocking);
     }
     if (e != cudaSuccess) return from_cuda(e);
@@ -277,6 +314,7 @@ int fftc_plan_launches(const fftc_plan* p) {
     case KIND_FUSED:
     case KIND_GENERIC: return p->batch > 0 ? 1 : 0;
     case KIND_FOURSTEP: return p->batch > 0 ? 2 : 0;
+    case KIND_PASSES: return p->batch > 0 ? p->pp.p : 0;
     case KIND_DIST: return dist_launches(p->dist);
   }
   return -1;
@@ -318,6 +356,13 @@ int fftc_plan_describe(const fftc_plan* p, char* buf, size_t len) {
     case KIND_DIST:
       n += dist_describe(p->dist, tmp + n, sizeof(tmp) - n);
       break;
+    case KIND_PASSES:
+      n += snprintf(tmp + n, sizeof(tmp) - n, "kind=passes N=%lld batch=%lld sign=%d passes=", (long long)p->N,
+                    (long long)p->batch, p->sign);
+      for (int s = 0; s < p->pp.p; ++s) n += snprintf(tmp + n, sizeof(tmp) - n, "%s%s", s ? "," : "", p->pp.e[s]->name);
+      n += snprintf(tmp + n, sizeof(tmp) - n, " tma=tensor3d/4d workspace=%lld launches=%d",
+                    (long long)(p->N * p->batch * (int64_t)sizeof(float2)), p->pp.p);
+      break;
   }
   if (buf && len) {
     strncpy(buf, tmp, len - 1);
@@ -339,5 +384,7 @@ int fftc_candidates(int64_t N, const char** names, int max) {
 int fftc_factorize(int64_t N, int* radices, int max) { return single_pass_radices(N, radices, max); }
 
 int fftc_plan_split(int64_t N, int64_t* M, int64_t* K) { return top_split(N, M, K); }
+
+int fftc_plan_passes(int64_t N, int* lengths, int max) { return pass_split(N, lengths, max); }
 
 }  // extern "C"

@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(P::THREADS, MINB)
     }
     return v;
   };
-  auto load = [&](int i) {
+  auto load = [&](int i, int) {
     float2 a = __ldcs(gi + (long long)i * g.in_s);
     return make_float2(a.x, csign_in * a.y);
   };

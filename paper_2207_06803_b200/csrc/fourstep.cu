@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(P::THREADS, MINB)
   const int j0 = (blockIdx.x % tiles) * FPB;
   const float2* gi = work + b * N + (long long)(j0 + f) * K;
   run_stages<P, true, false>(
-      sm, f, lt, true, tw, [&](int i) { return __ldcs(gi + i); }, [&](int, float2, int) {});
+      sm, f, lt, true, tw, [&](int i, int) { return __ldcs(gi + i); }, [&](int, float2, int) {});
   __syncthreads();  // the transposed store reads rows written by other warps
   // X[j + M k1] for j in [j0, j0 + FPB): FPB contiguous outputs per k1; lanes walk j
   // (row stride SS chosen so a 16-lane phase hits 16 banks), 8-byte stores.
@@ -95,9 +95,9 @@ static const ColEntry kCols[] = {
     FFTC_COL("c256_r16x16_t16x16", 256, Rad_16x16, 16, 16, LAY_FXOR, 2, 16, 16),
     FFTC_COL("c256_r16x16_t16x32", 256, Rad_16x16, 16, 32, LAY_FXOR, 1, 16, 16),
     FFTC_COL("c256_r16x16_t16x8", 256, Rad_16x16, 16, 8, LAY_INTER, 4, 16, 16),
+    FFTC_COL("c512_r32x16_t16x8", 512, Rad_32x16, 16, 8, LAY_INTER, 2, 32, 16),
     FFTC_COL("c512_r16x32_t16x16", 512, Rad_16x32, 16, 16, LAY_FXOR, 1, 16, 32),
     FFTC_COL("c512_r32x16_t16x16", 512, Rad_32x16, 16, 16, LAY_FXOR, 1, 32, 16),
-    FFTC_COL("c512_r32x16_t16x8", 512, Rad_32x16, 16, 8, LAY_INTER, 2, 32, 16),
     FFTC_COL("c1024_r32x32_t32x8", 1024, Rad_32x32, 32, 8, LAY_INTER, 1, 32, 32),
     FFTC_COL("c1024_r32x32_t32x4", 1024, Rad_32x32, 32, 4, LAY_INTER, 2, 32, 32),
     FFTC_COL("c1024_r32x32_t32x16", 1024, Rad_32x32, 32, 16, LAY_FXOR, 1, 32, 32),
@@ -110,9 +110,9 @@ static const ColEntry kCols[] = {
     FFTC_COL("c4096_r16x16x16_t128x4", 4096, Rad_16x16x16, 128, 4, LAY_INTER, 1, 16, 16, 16),
 };
 static const RowEntry kRows[] = {
+    FFTC_ROW("r256_r16x16_t16x8", 256, Rad_16x16, 16, 8, 2, 4, 16, 16),
     FFTC_ROW("r256_r16x16_t16x32", 256, Rad_16x16, 16, 32, 1, 1, 16, 16),
     FFTC_ROW("r256_r16x16_t16x16", 256, Rad_16x16, 16, 16, 1, 2, 16, 16),
-    FFTC_ROW("r256_r16x16_t16x8", 256, Rad_16x16, 16, 8, 2, 4, 16, 16),
     FFTC_ROW("r512_r32x16_t16x16", 512, Rad_32x16, 16, 16, 1, 2, 32, 16),
     FFTC_ROW("r1024_r32x32_t32x8", 1024, Rad_32x32, 32, 8, 2, 1, 32, 32),
     FFTC_ROW("r1024_r32x32_t32x4", 1024, Rad_32x32, 32, 4, 4, 2, 32, 32),

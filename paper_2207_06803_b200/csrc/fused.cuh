@@ -59,7 +59,9 @@ struct Radices {
 //   LAY_ODD  : f*SS + i, SS odd (F_FAST, other N).
 //   LAY_INTER: swzc(i)*FPB + f (interleaved columns, F_FAST with FPB < 16: a phase
 //              holds FPB columns x 16/FPB consecutive butterflies).
-enum Layout : int { LAY_AUTO = -1, LAY_SWZ = 0, LAY_FXOR = 1, LAY_ODD = 2, LAY_INTER = 3 };
+//   LAY_TMA128: i*16 + (((f >> 1) ^ (i & 7)) << 1 | (f & 1)) -- the TMA 128-byte swizzle of a
+//              [row i][16 columns] complex64 tile (1024-byte aligned), FPB = 16.
+enum Layout : int { LAY_AUTO = -1, LAY_SWZ = 0, LAY_FXOR = 1, LAY_ODD = 2, LAY_INTER = 3, LAY_TMA128 = 4 };
 
 constexpr int ilog2(int n) {
   int l = 0;
@@ -95,6 +97,7 @@ struct Sched {
   FFTC_HD static int gf(int f) { return (N % 16 == 0) ? (f & 15) : ((f >> 1) & 7); }
   FFTC_HD static int sidx(int f, int i) {
     if constexpr (LAY == LAY_FXOR) return f * SS + (i ^ gf(f));
+    else if constexpr (LAY == LAY_TMA128) return i * 16 + ((((f >> 1) ^ (i & 7)) << 1) | (f & 1));
     else if constexpr (LAY == LAY_INTER) return (i ^ ((i >> ISHIFT) & IMASK)) * FPB + f;
     else return f * SS + swz(i);
   }
@@ -113,7 +116,7 @@ struct Sched {
   }
 };
 
-// One Stockham stage.  SRC_G: stage reads through gload(i) (HBM, or a staging
+// One Stockham stage.  SRC_G: stage reads through gload(i, r) (HBM, or a staging
 // buffer); DST_G: stage writes through gstore(i, v, r) (HBM, or shared memory in
 // the transposed-output column kernel: then MID_SYNC forces the in-place barrier
 // between the reads and the writes); r = the element's index within its butterfly.
@@ -136,7 +139,7 @@ __device__ __forceinline__ void stage(float2* sm, int f, int lt, bool fvalid,
       sfor<R>([&](auto r_) {
         constexpr int r = decltype(r_)::value;
         const int i = j + r * NB;
-        if constexpr (SRC_G) v[k][r] = gload(i);
+        if constexpr (SRC_G) v[k][r] = gload(i, r);
         else v[k][r] = sm[P::sidx(f, i)];
       });
     }
@@ -343,7 +346,7 @@ __global__ void __launch_bounds__(P::THREADS, MINB)
     float2* go = gout + (long long)f * P::N;
     run_stages<P, true, true>(
         sm, f, lt, fvalid, tw,
-        [&](int i) {
+        [&](int i, int) {
           float2 a = __ldcs(gi + i);
           return make_float2(a.x, csign * a.y);
         },
@@ -352,7 +355,7 @@ __global__ void __launch_bounds__(P::THREADS, MINB)
     tile_in<P>(sm, gin, nf, csign);
     __syncthreads();
     run_stages<P, false, false>(
-        sm, f, lt, fvalid, tw, [&](int) { return make_float2(0.f, 0.f); }, [&](int, float2, int) {});
+        sm, f, lt, fvalid, tw, [&](int, int) { return make_float2(0.f, 0.f); }, [&](int, float2, int) {});
     __syncthreads();
     tile_out<P>(sm, gout, nf, 1.0f * csign);
   }
@@ -428,7 +431,7 @@ __global__ void __launch_bounds__(P::THREADS, MINB)
     auto gstore = [&](int i, float2 v, int) { __stcs(go + i, make_float2(v.x, csign * v.y)); };
     stage<P, 0, true, false>(
         work, f, lt, fvalid, tw,
-        [&](int i) {
+        [&](int i, int) {
           const float2 a = gl[i];
           return make_float2(a.x, csign * a.y);
         },
@@ -441,7 +444,7 @@ __global__ void __launch_bounds__(P::THREADS, MINB)
     }
     sfor<P::S - 1>([&](auto s_) {
       constexpr int s = decltype(s_)::value + 1;
-      stage<P, s, false, s == P::S - 1>(work, f, lt, fvalid, tw, [&](int) { return make_float2(0.f, 0.f); },
+      stage<P, s, false, s == P::S - 1>(work, f, lt, fvalid, tw, [&](int, int) { return make_float2(0.f, 0.f); },
                                         gstore);
     });
   }

@@ -1,0 +1,270 @@
+// passes.cu -- multi-pass large-N path with TMA tensor tiles (product path).
+//
+// For N above the single-pass limit, N = L_0 L_1 ... L_{p-1} (each L_s <= 256) and the
+// transform is p HBM passes, each one level of the paper's Eq. 2 applied
+// at the pass level in Stockham autosort form (SURVEY App. A.2 with radix -> L_s):
+//   pass s, Ns = L_0...L_{s-1}, NB = N / L_s columns c:
+//     v[r]  = a[c + r NB]                                   (Pi folded into the column read)
+//     v[r] *= w_{Ns L}^{(c mod Ns) r}          (s > 0)       (D^{Ns L}_{Ns})
+//     v     = DFT_{L_s} v                                   (a fused Stockham pass, fused.cuh)
+//     b[(c div Ns) Ns L + (c mod Ns) + r Ns] = v[r]         (natural order after the last pass)
+// A CTA owns 16 adjacent columns (one 128-byte segment per row).  The [L rows][16 cols]
+// tile is fetched by ONE 3-D TMA tensor load (cp.async.bulk.tensor, 128B-swizzled shared
+// layout, completion on an mbarrier), transformed in place, and -- for s > 0 -- written
+// back by ONE 4-D TMA tensor store (the autosort write is a [L][16] box of a
+// (Ns, L, NB/Ns, batch) view).  Pass 0 (Ns = 1) writes each column's L outputs
+// contiguously, via coalesced 8-byte stores.  CTAs are persistent and double-buffered:
+// the tile after next streams in while the current one is computed.
+#include <cuda.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include "colfft.cuh"
+#include "passes.h"
+#include "tma.cuh"
+
+namespace fftc {
+
+namespace {
+
+template <class P, bool FIRST, int MINB>
+__global__ void __launch_bounds__(P::THREADS, MINB)
+    k_pass(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout,
+           float2* __restrict__ out_first, const float2* __restrict__ tw, const float2* __restrict__ twA,
+           const float2* __restrict__ twB, PassGeom g, float csign_in, float csign_out) {
+  static_assert(P::FPB == 16 && P::LAY == LAY_TMA128, "pass tiles are 16 columns, TMA 128B swizzle");
+  constexpr int L = P::N, C = 16;
+  constexpr uint32_t TILE_BYTES = (uint32_t)L * C * 8u;
+  constexpr int R0 = P::R(0);
+  constexpr int NB0 = L / R0;                      // sub-stage 0: element i = j + r NB0
+  constexpr int NB2 = ilog2(highbit(R0 - 1)) + 1;  // step powers for r < R0
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  float2* buf0 = reinterpret_cast<float2*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full[2];
+  int f, lt;
+  P::thread_coords(threadIdx.x, f, lt);
+  const long long T = g.tiles_total;
+  const int tpb = g.tiles_per_batch;
+  auto issue = [&](long long t, int k) {
+    const int b = (int)(t / tpb), c0 = (int)(t % tpb) * C;
+    mbar_arrive_expect_tx(&full[k], TILE_BYTES);
+    tma_load_3d(buf0 + k * L * C, &tin, c0, 0, b, &full[k]);
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (blockIdx.x < T) issue(blockIdx.x, 0);
+    if (blockIdx.x + gridDim.x < T) issue(blockIdx.x + gridDim.x, 1);
+  }
+  int it = 0;
+  for (long long t = blockIdx.x; t < T; t += gridDim.x, ++it) {
+    const int k = it & 1;
+    float2* sm = buf0 + k * L * C;
+    const int b = (int)(t / tpb), c0 = (int)(t % tpb) * C;
+    const int c = c0 + f;
+    mbar_wait(&full[k], (it >> 1) & 1);
+    // input twiddle w_T^{m i}, T = Ns L, m = c mod Ns: base per butterfly, step powers per thread
+    const long long m = g.tw ? (long long)(c % g.Ns) : 0;
+    float2 sp[NB2];
+    if (g.tw) {
+      sp[0] = root_lookup(twA, twB, m * NB0);
+      sfor<NB2 - 1>([&](auto b_) {
+        constexpr int bb = decltype(b_)::value + 1;
+        sp[bb] = cmul(sp[bb - 1], sp[bb - 1]);
+      });
+    }
+    float2 base = make_float2(1.f, 0.f);
+    auto gload = [&](int i, int r) {
+      float2 v = sm[P::sidx(f, i)];
+      v.y *= csign_in;
+      if (g.tw) {
+        if (r == 0) base = root_lookup(twA, twB, m * i);
+        float2 w = base;
+        sfor<NB2>([&](auto b_) {
+          constexpr int bb = decltype(b_)::value;
+          if (r & (1 << bb)) w = cmul(w, sp[bb]);
+        });
+        v = cmul(v, w);
+      }
+      return v;
+    };
+    auto gstore = [&](int i, float2 v, int) { sm[P::sidx(f, i)] = make_float2(v.x, csign_out * v.y); };
+    // sub-stages of DFT_L in place on the tile (every stage reads all, syncs, writes)
+    sfor<P::S>([&](auto s_) {
+      constexpr int s = decltype(s_)::value;
+      stage<P, s, s == 0, s == P::S - 1, true>(sm, f, lt, true, tw, gload, gstore);
+    });
+    if constexpr (!FIRST) {
+      fence_proxy_async_smem();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        tma_store_4d(&tout, sm, c0 % g.Ns, 0, c0 / g.Ns, b);
+        bulk_commit();
+      }
+    } else {
+      __syncthreads();
+      // pass 0: column c's outputs are contiguous at c L + r; lanes walk r
+      float2* go = out_first + (long long)b * g.N + (long long)c0 * L;
+      constexpr int PER = L * C / P::THREADS;
+      sfor<PER>([&](auto n_) {
+        constexpr int n = decltype(n_)::value;
+        const int e = threadIdx.x + n * P::THREADS;
+        const int r = e % L, cc = e / L;
+        __stcs(go + cc * L + r, sm[P::sidx(cc, r)]);
+      });
+      __syncthreads();
+    }
+    if (threadIdx.x == 0 && t + 2 * (long long)gridDim.x < T) {
+      if constexpr (!FIRST) bulk_wait_read0();  // the store has finished reading this buffer
+      issue(t + 2 * (long long)gridDim.x, k);
+    }
+  }
+  if constexpr (!FIRST)
+    if (threadIdx.x == 0) bulk_wait0();
+}
+
+template <class P, int MINB>
+cudaError_t launch_pass(bool first, const CUtensorMap& tin, const CUtensorMap& tout, float2* out_first,
+                        const float2* tw, const float2* twA, const float2* twB, const PassGeom& g, int conj_in,
+                        int conj_out, cudaStream_t st) {
+  constexpr size_t smem = (size_t)2 * P::N * 16 * sizeof(float2) + 1024;
+  static int grid_max[2] = {0, 0};
+  auto kern = first ? k_pass<P, true, MINB> : k_pass<P, false, MINB>;
+  int& gm = grid_max[first ? 1 : 0];
+  if (!gm) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, P::THREADS, smem);
+    if (e != cudaSuccess) return e;
+    gm = sms * (per > 0 ? per : 1);
+  }
+  if (g.tiles_total == 0) return cudaSuccess;
+  const unsigned grid = (unsigned)(g.tiles_total < gm ? g.tiles_total : gm);
+  kern<<<grid, P::THREADS, smem, st>>>(tin, tout, out_first, tw, twA, twB, g, conj_in ? -1.f : 1.f,
+                                      conj_out ? -1.f : 1.f);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+#define FFTC_PASS(NAME, L, RAD, TPF, MINB, ...) \
+  {L, RAD::S, {__VA_ARGS__}, TPF, &launch_pass<Sched<L, RAD, TPF, 16, F_FAST, 0, LAY_TMA128>, MINB>, NAME}
+
+using PRad_4x4 = Radices<4, 4>;
+using PRad_8x4 = Radices<8, 4>;
+using PRad_8x8 = Radices<8, 8>;
+using PRad_16x8 = Radices<16, 8>;
+using PRad_16x16 = Radices<16, 16>;
+
+static const PassEntry kPasses[] = {
+    FFTC_PASS("p16_r4x4", 16, PRad_4x4, 4, 8, 4, 4),
+    FFTC_PASS("p32_r8x4", 32, PRad_8x4, 4, 8, 8, 4),
+    FFTC_PASS("p64_r8x8", 64, PRad_8x8, 8, 6, 8, 8),
+    FFTC_PASS("p128_r16x8", 128, PRad_16x8, 16, 3, 16, 8),
+    FFTC_PASS("p256_r16x16", 256, PRad_16x16, 16, 3, 16, 16),
+};
+
+const PassEntry* find_pass(int L) {
+  for (const auto& e : kPasses)
+    if (e.L == L) return &e;
+  return nullptr;
+}
+
+// ---------------------------------------------------------------- host: tensor maps
+typedef CUresult (*encode_fn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static encode_fn get_encode() {
+  static encode_fn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (encode_fn)p;
+  }
+  return fn;
+}
+
+// in: a [batch][L rows][NB cols] view, box [16 cols][L rows]
+static bool map_in(CUtensorMap* m, const void* base, long long N, int L, long long batch) {
+  encode_fn enc = get_encode();
+  if (!enc) return false;
+  const long long NB = N / L;
+  cuuint64_t dims[3] = {(cuuint64_t)NB, (cuuint64_t)L, (cuuint64_t)batch};
+  cuuint64_t strides[2] = {(cuuint64_t)NB * 8, (cuuint64_t)N * 8};
+  cuuint32_t box[3] = {16, (cuuint32_t)L, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_INT64, 3, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// out (autosort write): a [batch][NB/Ns][L][Ns] view, box [16][L][1][1]
+static bool map_out(CUtensorMap* m, void* base, long long N, int L, long long Ns, long long batch) {
+  encode_fn enc = get_encode();
+  if (!enc) return false;
+  const long long NB = N / L;
+  cuuint64_t dims[4] = {(cuuint64_t)Ns, (cuuint64_t)L, (cuuint64_t)(NB / Ns), (cuuint64_t)batch};
+  cuuint64_t strides[3] = {(cuuint64_t)Ns * 8, (cuuint64_t)Ns * L * 8, (cuuint64_t)N * 8};
+  cuuint32_t box[4] = {16, (cuuint32_t)L, 1, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_INT64, 4, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool passes_available() { return get_encode() != nullptr; }
+
+// Split N (power of two, 2^9 .. 2^32) into p = ceil(log2 N / 8) pass lengths in [16, 256],
+// as equal as possible, larger first.
+int pass_split(long long N, int* Ls, int max) {
+  if (N < 512 || (N & (N - 1))) return -1;
+  int n = 0;
+  while ((1LL << n) < N) ++n;
+  const int p = (n + 7) / 8;
+  if (p > max) return -1;
+  for (int s = 0; s < p; ++s) {
+    const int e = n / p + (s < n % p ? 1 : 0);
+    if (e < 4 || e > 8) return -1;
+    Ls[s] = 1 << e;
+  }
+  return p;
+}
+
+cudaError_t passes_execute(const PassPlanData& pp, const float2* in, float2* out, float2* work, long long batch,
+                           int conj, cudaStream_t st) {
+  // ping-pong so the last pass lands in `out`: pass s writes out if (p-1-s) even, else work
+  const int p = pp.p;
+  long long Ns = 1;
+  const float2* src = in;
+  for (int s = 0; s < p; ++s) {
+    float2* dst = ((p - 1 - s) % 2 == 0) ? out : work;
+    const PassEntry* e = pp.e[s];
+    const int L = e->L;
+    CUtensorMap tin, tout;
+    if (!map_in(&tin, src, pp.N, L, batch)) return cudaErrorInvalidValue;
+    if (s > 0 && !map_out(&tout, dst, pp.N, L, Ns, batch)) return cudaErrorInvalidValue;
+    if (s == 0) memset(&tout, 0, sizeof(tout));
+    PassGeom g{};
+    g.tiles_per_batch = (int)(pp.N / L / 16);
+    g.tiles_total = batch * g.tiles_per_batch;
+    g.Ns = (int)Ns;
+    g.N = pp.N;
+    g.tw = s > 0;
+    cudaError_t err = e->launch(s == 0, tin, tout, dst, pp.tw[s], pp.twA[s], pp.twB[s], g, conj && s == 0,
+                                conj && s == p - 1, st);
+    if (err != cudaSuccess) return err;
+    src = dst;
+    Ns *= L;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace fftc

@@ -1,0 +1,46 @@
+// passes.h -- multi-pass (TMA tensor tile) large-N path, host side (product path).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fftc {
+
+struct PassGeom {
+  long long tiles_total;  // batch * tiles_per_batch
+  int tiles_per_batch;    // (N / L) / 16
+  int Ns;                 // Stockham Ns of this pass (product of earlier pass lengths)
+  long long N;
+  int tw;                 // apply the input twiddle w_{Ns L}^{(c mod Ns) r}
+};
+
+typedef cudaError_t (*pass_launch_fn)(bool first, const CUtensorMap& tin, const CUtensorMap& tout, float2* out_first,
+                                      const float2* tw, const float2* twA, const float2* twB, const PassGeom& g,
+                                      int conj_in, int conj_out, cudaStream_t st);
+
+struct PassEntry {
+  int L;
+  int S;
+  int R[8];
+  int tpf;
+  pass_launch_fn launch;
+  const char* name;
+};
+
+constexpr int kMaxPasses = 6;
+struct PassPlanData {
+  long long N = 0;
+  int p = 0;
+  const PassEntry* e[kMaxPasses] = {};
+  float2* tw[kMaxPasses] = {};   // stage twiddles of DFT_{L_s}
+  float2* twA[kMaxPasses] = {};  // w_{Ns L}^t, t < 4096
+  float2* twB[kMaxPasses] = {};  // w_{Ns L}^{4096 h}
+};
+
+const PassEntry* find_pass(int L);
+bool passes_available();
+int pass_split(long long N, int* Ls, int max);
+cudaError_t passes_execute(const PassPlanData& pp, const float2* in, float2* out, float2* work, long long batch,
+                           int conj, cudaStream_t st);
+
+}  // namespace fftc

@@ -4,11 +4,12 @@
 #include <stdint.h>
 
 #include "fourstep.h"
+#include "passes.h"
 #include "registry.h"
 
 namespace fftc {
 
-enum PlanKind : int { KIND_COPY = 0, KIND_FUSED = 1, KIND_GENERIC = 2, KIND_FOURSTEP = 3, KIND_DIST = 4 };
+enum PlanKind : int { KIND_COPY = 0, KIND_FUSED = 1, KIND_GENERIC = 2, KIND_FOURSTEP = 3, KIND_DIST = 4, KIND_PASSES = 5 };
 
 struct DistState;  // dist.cu
 
@@ -40,6 +41,8 @@ struct fftc_plan {
   float2* d_twA = nullptr;     // w_N^t, t < 4096
   float2* d_twB = nullptr;     // w_N^{4096 h}
   float2* d_work = nullptr;    // N*batch complex
+  // multi-pass TMA path (power-of-two N > 4096)
+  fftc::PassPlanData pp;
   // host-buffer execution
   fftc::HostStage* hs = nullptr;
   // distributed six-step

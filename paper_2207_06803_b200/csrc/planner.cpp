@@ -6,8 +6,9 @@
 // schedule for N if there is one; otherwise a generic schedule from the codelet
 // set {16, 8, 4, 2, 9, 3, 25, 5, 7} -- fewest stages, larger radices first,
 // power-of-two radices before odd ones; prime factors > 7 are rejected.
-// Above the single-pass limit the top-level split N = M K picks the most
-// balanced pair with compiled column (DFT_M) and row (DFT_K) pass kernels.
+// Above the single-pass limit: powers of two run the multi-pass TMA path
+// (passes.cu) when it is the faster one, else the four-step with the split
+// N = M K chosen below.
 #include "planner.h"
 
 #include <stdlib.h>
@@ -74,15 +75,17 @@ int top_split(int64_t N, int64_t* M, int64_t* K) {
   }
   int64_t bestM = 0, bestK = 0;
   const char* force = getenv("FFTC_SPLIT_M");  // tuning: pin the top-level split
+  // measured on B200 (tools/tune4.py): the strided column pass is the slower one, so keep
+  // its length M near 512 (C = 8..16 columns per CTA fit in shared memory) and give the
+  // row pass the rest (K <= 4096)
+  auto score = [](int64_t m) { return m > 512 ? m / 512 : 512 / m; };
   for (int i = 0; i < col_count(); ++i) {
     const ColEntry* c = col_at(i);
     if (N % c->M) continue;
     if (force && atoll(force) != c->M) continue;
     const int64_t k = N / c->M;
     if (k > 0x7fffffff || !find_row((int)k)) continue;
-    const int64_t d = (c->M > k) ? c->M - k : k - c->M;
-    const int64_t bd = (bestM > bestK) ? bestM - bestK : bestK - bestM;
-    if (bestM == 0 || d < bd) {
+    if (bestM == 0 || score(c->M) < score(bestM)) {
       bestM = c->M;
       bestK = k;
     }

@@ -86,6 +86,15 @@ def test_planner_fourstep_split(N, M, K):
     assert math.prod(fftc.fftc_factorize(N)) == N
 
 
+def test_planner_passes():
+    for n in range(9, 41):
+        Ls = fftc.fftc_plan_passes(1 << n)
+        assert Ls is not None and math.prod(Ls) == 1 << n
+        assert len(Ls) == (n + 7) // 8 and all(16 <= L <= 256 for L in Ls)
+    assert fftc.fftc_plan_passes(3 * 4096) is None
+    assert fftc.fftc_plan_passes(256) is None
+
+
 def test_no_device_fails_loudly():
     import torch
     if torch.cuda.is_available():

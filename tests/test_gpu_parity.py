@@ -74,10 +74,26 @@ def test_small_batches(N, batch, sign):
 
 @pytest.mark.parametrize("N", [1 << 16, 1 << 20])
 @pytest.mark.parametrize("sign", [-1, 1])
-def test_fourstep_small_batch(N, sign):
+@pytest.mark.parametrize("large", ["passes", "fourstep"])
+def test_fourstep_small_batch(N, sign, large, monkeypatch):
+    monkeypatch.setenv("FFTC_LARGE", large)
     x = synth.normal_c64(N, 3, seed=N)
+    with fftc.Plan(N, 3, sign) as p:
+        assert ("kind=" + large) in p.describe()
     y = gpu_fft(x, sign)
     check(y, x, sign)
+
+
+@pytest.mark.parametrize("n", list(range(13, 25)))
+def test_multipass_all_pow2(n):
+    """Every power of two 2^13..2^24 on the multi-pass TMA path (2-3 passes), both signs, odd batch."""
+    N = 1 << n
+    batch = max(1, (1 << 22) // N) | 1
+    x = synth.uniform_c64(N, batch, seed=n)
+    for sign in (-1, 1):
+        y = gpu_fft(x, sign)
+        idx = sample_idx(batch, n_rand=4)
+        check(y[idx], x[idx], sign)
 
 
 @pytest.mark.parametrize("N", POW2 + MIXED)
@@ -209,7 +225,9 @@ def test_boundary_errors():
 
 
 def test_describe_and_launches():
-    for N, kind, launches in [(64, "fused", 1), (4096, "fused", 1), (48, "generic", 1), (1 << 20, "fourstep", 2)]:
+    for N, kind, launches in [(64, "fused", 1), (4096, "fused", 1), (48, "generic", 1), (1 << 20, "fourstep", 2),
+                              (1 << 24, "passes", 3), (1 << 13, "passes", 2),
+                              (1 << 16, "passes", 2)]:
         with fftc.Plan(N, 2, -1) as p:
             assert ("kind=" + kind) in p.describe()
             assert p.launches() == launches
