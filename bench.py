@@ -254,6 +254,32 @@ def run_fftc(args):
               "algorithmic_bytes_per_launch": bytes_mean, "peak_source": peak_kind}
     clocks = sampler.summary()
 
+    # launch-latency-bound workloads: the same step captured in a CUDA graph (reps steps per replay)
+    graph = None
+    if args.graph or args.workload == "c1":
+        reps = 50
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(stream)
+        with torch.cuda.stream(side):
+            one_step()  # warm on the capture stream
+            torch.cuda.synchronize(dev)
+            with torch.cuda.graph(g, stream=side):
+                for _ in range(reps):
+                    one_step()
+        torch.cuda.synchronize(dev)
+        g.replay()
+        torch.cuda.synchronize(dev)
+        ga, gb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ga.record(stream)
+        for _ in range(K):
+            g.replay()
+        gb.record(stream)
+        torch.cuda.synchronize(dev)
+        gt = ga.elapsed_time(gb) / 1e3 / (K * reps)
+        graph = {"ms_per_step": round(gt * 1e3, 5), "value": round(step_flops / gt / 1e9, 2), "unit": UNIT,
+                 "steps_per_graph": reps, "note": "CUDA graph replay of %d steps; device time per step" % reps}
+
     # e2e through the C ABI on host buffers (pinned), H2D + kernels + D2H inside the timed region
     e2e = None
     if not args.no_e2e:
@@ -295,6 +321,8 @@ def run_fftc(args):
             "roofline": rl, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_per_step * K,
             "clocks": clocks, "per_job": per_job,
         }
+        if graph:
+            line["graph"] = graph
         print(json.dumps(line), flush=True)
     for p in plans:
         p.close()
@@ -401,6 +429,7 @@ def main():
     ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--c5-n", type=int, default=1 << 30)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--graph", action="store_true", help="also time the step captured in a CUDA graph")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-budget", type=float, default=10.0)

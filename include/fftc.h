@@ -129,8 +129,9 @@ int fftc_plan_passes(int64_t N, int* lengths, int max);
 fftc_status fftc_dist_get_unique_id(void* id_out);
 
 /* Collective over `nranks` processes; each calls it with the same N, sign
- * and id and its own rank, with its GPU current.  nranks == 1 is allowed
- * (no communicator; local transposes).  Returns NULL on failure.
+ * and id and its own rank, with its GPU current.  nranks == 1 without
+ * loopback returns the single-GPU plan for N (the all-to-alls would be
+ * identities).  Returns NULL on failure.
  * `loopback` != 0 runs all nranks virtual ranks inside this one process on
  * the current GPU (the all-to-alls become device copies; id/rank ignored):
  * in/out then hold the whole N-element vector.                            */

@@ -313,6 +313,9 @@ extern "C" fftc_plan* fftc_dist_plan_create(int64_t N, int sign, const void* ncc
   if (N < 2 || (sign != -1 && sign != 1) || nranks < 1 || (!loopback && (rank < 0 || rank >= nranks)))
     return fail(FFTC_ERROR_INVALID_VALUE, nullptr);
   if (!loopback && nranks > 1 && !nccl_id) return fail(FFTC_ERROR_INVALID_VALUE, nullptr);
+  // One rank without loopback: every all-to-all is the identity, so the transform is
+  // the single-GPU plan (multi-pass / four-step / fused) -- no copies, no extra passes.
+  if (nranks == 1 && !loopback && !getenv("FFTC_DIST_SIXSTEP")) return fftc_plan_create(N, 1, sign);
   int dev = 0;
   fftc_status ds = fftc_check_device(&dev);
   if (ds != FFTC_SUCCESS) return fail(ds, nullptr);

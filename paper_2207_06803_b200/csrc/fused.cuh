@@ -85,7 +85,7 @@ struct Sched {
                              : (MAP == LT_FAST) ? LAY_SWZ
                              : (PAD_ == 0 && (N % 16 == 0 || N == 8)) ? LAY_FXOR : LAY_ODD;
   static constexpr bool FXOR = (LAY == LAY_FXOR);
-  static constexpr bool SWZ = (LAY == LAY_SWZ) && (N % 16 == 0);
+  static constexpr bool SWZ = (LAY == LAY_SWZ) && ((N + PAD_) % 16 == 0);
   static constexpr int SS = (LAY == LAY_FXOR) ? N : (LAY == LAY_ODD) ? ((N + PAD_) | 1) : (N + PAD_);
   static constexpr size_t SMEM = size_t(LAY == LAY_INTER ? N : SS) * FPB * sizeof(float2);
   // LAY_INTER: XOR the bank bits of i (mod 16/FPB) with the bits above the leaf radix

@@ -9,6 +9,11 @@ namespace fftc {
   {N, RAD::S, {__VA_ARGS__}, TPF, FPB, TPF * FPB, DIRECT,                                        \
    Sched<N, RAD, TPF, FPB, MAP>::SMEM, &launch_fused_batch<Sched<N, RAD, TPF, FPB, MAP>, DIRECT, MINB>, \
    NAME}
+// LT_FAST with the row padded to a multiple of 16 so the XOR swizzle applies to any N
+#define FFTC_ENTRY_PAD(NAME, N, RAD, TPF, FPB, PAD, MINB, ...)                                  \
+  {N, RAD::S, {__VA_ARGS__}, TPF, FPB, TPF * FPB, true,                                        \
+   Sched<N, RAD, TPF, FPB, LT_FAST, PAD>::SMEM, &launch_fused_batch<Sched<N, RAD, TPF, FPB, LT_FAST, PAD>, true, MINB>, \
+   NAME}
 // persistent, TMA-fed variant (LT_FAST schedules)
 #define FFTC_TMA(NAME, N, RAD, TPF, FPB, MINB, ...)                                               \
   {N, RAD::S, {__VA_ARGS__}, TPF, FPB, TPF * FPB, 2, Sched<N, RAD, TPF, FPB, LT_FAST>::SMEM * 2,    \
@@ -48,6 +53,9 @@ using Rad_8x8x8x8 = Radices<8, 8, 8, 8>;
 using Rad_15x14 = Radices<15, 14>;
 using Rad_3x27x27 = Radices<3, 27, 27>;
 using Rad_25x25x5 = Radices<25, 25, 5>;
+using Rad_6x35 = Radices<6, 35>;
+using Rad_27x9x9 = Radices<27, 9, 9>;
+using Rad_9x27x9 = Radices<9, 27, 9>;
 using Rad_15x4 = Radices<15, 4>;
 using Rad_15x7 = Radices<15, 7>;
 using Rad_7x30 = Radices<7, 30>;

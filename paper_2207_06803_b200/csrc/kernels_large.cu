@@ -16,12 +16,10 @@ const FusedEntry kTable_large[] = {
     FFTC_ENTRY("n4096_r16x16x16_t128x1", 4096, Rad_16x16x16, 128, 1, LT_FAST, true, 4, 16, 16, 16),
     FFTC_ENTRY("n4096_r16x16x16_t256x1", 4096, Rad_16x16x16, 256, 1, LT_FAST, true, 3, 16, 16, 16),
     FFTC_TMA("n4096_r16x16x16_t256x1_tma", 4096, Rad_16x16x16, 256, 1, 3, 16, 16, 16),
-    FFTC_ENTRY("n2048_r16x16x8_t256x1", 2048, Rad_16x16x8, 256, 1, LT_FAST, true, 4, 16, 16, 8),
-    FFTC_ENTRY("n2048_r16x8x16_t128x1", 2048, Rad_16x8x16, 128, 1, LT_FAST, true, 6, 16, 8, 16),
     FFTC_ENTRY("n4096_r16x16x16_t128x1m6", 4096, Rad_16x16x16, 128, 1, LT_FAST, true, 5, 16, 16, 16),
-    FFTC_ENTRY("n4096_r16x32x8_t256x1", 4096, Rad_16x32x8, 256, 1, LT_FAST, true, 3, 16, 32, 8),
-    FFTC_ENTRY("n4096_r8x32x16_t256x1", 4096, Rad_8x32x16, 256, 1, LT_FAST, true, 3, 8, 32, 16),
-    FFTC_ENTRY("n4096_r8x8x8x8_t512x1", 4096, Rad_8x8x8x8, 512, 1, LT_FAST, true, 2, 8, 8, 8, 8),
+    FFTC_ENTRY("n4096_r16x16x16_t256x1m2", 4096, Rad_16x16x16, 256, 1, LT_FAST, true, 2, 16, 16, 16),
+    FFTC_ENTRY("n4096_r16x16x16_t128x1m4", 4096, Rad_16x16x16, 128, 1, LT_FAST, true, 4, 16, 16, 16),
+    FFTC_ENTRY("n4096_r16x16x16_t128x1m3", 4096, Rad_16x16x16, 128, 1, LT_FAST, true, 3, 16, 16, 16),
 };
 const int kCount_large = (int)(sizeof(kTable_large) / sizeof(kTable_large[0]));
 
