@@ -80,6 +80,8 @@ cudaError_t exec_local(const fftc_plan* p, const float2* in, float2* out, long l
       return launch_generic(p->gs, in, out, p->d_tw, batch, conj, st);
     case KIND_PASSES:
       return passes_execute(p->pp, in, out, work, batch, conj, st);
+    case KIND_L2:
+      return l2_execute(p->l2, in, out, work, batch, conj, st);
     case KIND_FOURSTEP: {
       const ColGeom g = fourstep_cols_geom(p->ce, p->N, p->K);
       cudaError_t e = p->ce->launch(in, work, p->d_tw, p->d_twA, p->d_twB, g, batch, conj, 0, st);
@@ -108,6 +110,11 @@ static void free_plan(fftc_plan* p) {
   cudaFree(p->d_twA);
   cudaFree(p->d_twB);
   cudaFree(p->d_work);
+  for (int s = 0; s < kMaxL2Passes; ++s) {
+    cudaFree(p->l2.tw[s]);
+    cudaFree(p->l2.twA[s]);
+    cudaFree(p->l2.twB[s]);
+  }
   for (int s = 0; s < kMaxPasses; ++s) {
     cudaFree(p->pp.tw[s]);
     cudaFree(p->pp.twA[s]);
@@ -184,13 +191,46 @@ fftc_plan* fftc_plan_create(int64_t N, int64_t batch, int sign) {
     if (err != cudaSuccess) return fail(p, from_cuda(err));
     return p;
   }
+  const char* large = getenv("FFTC_LARGE");
+  // L2-resident multi-pass path (FFTC_LARGE=l2): powers of two 2^13..2^21, one HBM round
+  // trip.  Measured on B200 (profiles/r01d): the pass tiles are issue-bound (~60 thread
+  // instructions per element per pass), so running all passes in one kernel does not beat
+  // the HBM multi-pass kernels yet; it is opt-in until the tile compute is cheaper.
+  {
+    int Ls2[kMaxL2Passes];
+    const int np2 = l2_split(N, Ls2, kMaxL2Passes);
+    const L2Entry* e2 = np2 > 0 ? find_l2(Ls2, np2) : nullptr;
+    const bool want = large && strcmp(large, "l2") == 0;
+    if (e2 && want && passes_available()) {
+      p->kind = KIND_L2;
+      L2PlanData& d = p->l2;
+      d.N = N;
+      d.p = np2;
+      d.e = e2;
+      l2_geometry(N, batch, np2, &d.tc, &d.slots, &d.lag);
+      int64_t Ns = 1;
+      for (int s = 0; s < np2 && err == cudaSuccess; ++s) {
+        d.L[s] = Ls2[s];
+        const PassEntry* pe = find_pass(Ls2[s]);  // same radices as the HBM pass kernel of this length
+        if (!pe) return fail(p, FFTC_ERROR_UNSUPPORTED_SIZE);
+        const int64_t T = Ns * Ls2[s];
+        d.tw[s] = upload_stage_table(Ls2[s], pe->R, pe->S, &err);
+        if (err == cudaSuccess) d.twA[s] = upload_root_table(T, T < 4096 ? T : 4096, 1, &err);
+        if (err == cudaSuccess) d.twB[s] = upload_root_table(T, (T + 4095) / 4096, 4096, &err);
+        Ns = T;
+      }
+      if (err == cudaSuccess && batch > 0) err = cudaMalloc(&p->d_work, l2_work_bytes(d, batch));
+      if (err != cudaSuccess) return fail(p, from_cuda(err));
+      return p;
+    }
+  }
   // multi-pass TMA path for powers of two (FFTC_LARGE=fourstep selects the two-pass kernels)
   int Ls[kMaxPasses];
-  const char* large = getenv("FFTC_LARGE");
   const int np = pass_split(N, Ls, kMaxPasses);
-  // measured on B200: two TMA passes beat the four-step at 2^16; at 2^17..2^23 the
-  // four-step's two passes beat three TMA passes; from 2^24 the TMA passes win
-  bool use_passes = np > 0 && passes_available() && (np == 2 || split < 0 || N >= ((int64_t)1 << 24));
+  // measured on B200 (profiles/r01d): with shared-state-space tile addressing the TMA passes
+  // beat the four-step at every power of two above 4096 (2^20: three passes 2.37 ms vs the
+  // 512 x 2048 four-step 2.55 ms per 2^28 elements)
+  bool use_passes = np > 0 && passes_available();
   if (large && strcmp(large, "fourstep") == 0) use_passes = false;
   if (large && strcmp(large, "passes") == 0 && np > 0 && passes_available()) use_passes = true;
   if (use_passes) {
@@ -266,6 +306,7 @@ fftc_status fftc_execute_host(fftc_plan* p, const void* host_in, void* host_out)
       if (e == cudaSuccess) e = cudaMalloc(&hs->d_out[i], (size_t)(chunk * tbytes));
       if (e == cudaSuccess && (p->kind == KIND_FOURSTEP || p->kind == KIND_PASSES))
         e = cudaMalloc(&hs->d_work[i], (size_t)(chunk * tbytes));
+      if (e == cudaSuccess && p->kind == KIND_L2) e = cudaMalloc(&hs->d_work[i], l2_work_bytes(p->l2, chunk));
       if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&hs->st[i], cudaStreamNonBlocking);
     }
     if (e != cudaSuccess) return from_cuda(e);
@@ -315,6 +356,7 @@ int fftc_plan_launches(const fftc_plan* p) {
     case KIND_GENERIC: return p->batch > 0 ? 1 : 0;
     case KIND_FOURSTEP: return p->batch > 0 ? 2 : 0;
     case KIND_PASSES: return p->batch > 0 ? p->pp.p : 0;
+    case KIND_L2: return p->batch > 0 ? 1 : 0;
     case KIND_DIST: return dist_launches(p->dist);
   }
   return -1;
@@ -355,6 +397,13 @@ int fftc_plan_describe(const fftc_plan* p, char* buf, size_t len) {
       break;
     case KIND_DIST:
       n += dist_describe(p->dist, tmp + n, sizeof(tmp) - n);
+      break;
+    case KIND_L2:
+      n += snprintf(tmp + n, sizeof(tmp) - n, "kind=l2 N=%lld batch=%lld sign=%d passes=", (long long)p->N,
+                    (long long)p->batch, p->sign);
+      for (int s = 0; s < p->l2.p; ++s) n += snprintf(tmp + n, sizeof(tmp) - n, "%s%d", s ? "x" : "", p->l2.L[s]);
+      n += snprintf(tmp + n, sizeof(tmp) - n, " kernel=%s chunk=%d ring_slots=%d lag=%d workspace=%lld launches=1",
+                    p->l2.e->name, p->l2.tc, p->l2.slots, p->l2.lag, (long long)l2_work_bytes(p->l2, p->batch));
       break;
     case KIND_PASSES:
       n += snprintf(tmp + n, sizeof(tmp) - n, "kind=passes N=%lld batch=%lld sign=%d passes=", (long long)p->N,

@@ -19,8 +19,8 @@
 #include <stdlib.h>
 #include <string.h>
 
-#include "colfft.cuh"
 #include "passes.h"
+#include "passtile.cuh"
 #include "tma.cuh"
 
 namespace fftc {
@@ -35,11 +35,8 @@ __global__ void __launch_bounds__(P::THREADS, MINB)
   static_assert(P::FPB == 16 && P::LAY == LAY_TMA128, "pass tiles are 16 columns, TMA 128B swizzle");
   constexpr int L = P::N, C = 16;
   constexpr uint32_t TILE_BYTES = (uint32_t)L * C * 8u;
-  constexpr int R0 = P::R(0);
-  constexpr int NB0 = L / R0;                      // sub-stage 0: element i = j + r NB0
-  constexpr int NB2 = ilog2(highbit(R0 - 1)) + 1;  // step powers for r < R0
   extern __shared__ __align__(1024) unsigned char smraw[];
-  float2* buf0 = reinterpret_cast<float2*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  float2* buf0 = reinterpret_cast<float2*>(smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u));
   __shared__ __align__(8) uint64_t full[2];
   int f, lt;
   P::thread_coords(threadIdx.x, f, lt);
@@ -66,37 +63,7 @@ __global__ void __launch_bounds__(P::THREADS, MINB)
     const int b = (int)(t / tpb), c0 = (int)(t % tpb) * C;
     const int c = c0 + f;
     mbar_wait(&full[k], (it >> 1) & 1);
-    // input twiddle w_T^{m i}, T = Ns L, m = c mod Ns: base per butterfly, step powers per thread
-    const long long m = g.tw ? (long long)(c % g.Ns) : 0;
-    float2 sp[NB2];
-    if (g.tw) {
-      sp[0] = root_lookup(twA, twB, m * NB0);
-      sfor<NB2 - 1>([&](auto b_) {
-        constexpr int bb = decltype(b_)::value + 1;
-        sp[bb] = cmul(sp[bb - 1], sp[bb - 1]);
-      });
-    }
-    float2 base = make_float2(1.f, 0.f);
-    auto gload = [&](int i, int r) {
-      float2 v = sm[P::sidx(f, i)];
-      v.y *= csign_in;
-      if (g.tw) {
-        if (r == 0) base = root_lookup(twA, twB, m * i);
-        float2 w = base;
-        sfor<NB2>([&](auto b_) {
-          constexpr int bb = decltype(b_)::value;
-          if (r & (1 << bb)) w = cmul(w, sp[bb]);
-        });
-        v = cmul(v, w);
-      }
-      return v;
-    };
-    auto gstore = [&](int i, float2 v, int) { sm[P::sidx(f, i)] = make_float2(v.x, csign_out * v.y); };
-    // sub-stages of DFT_L in place on the tile (every stage reads all, syncs, writes)
-    sfor<P::S>([&](auto s_) {
-      constexpr int s = decltype(s_)::value;
-      stage<P, s, s == 0, s == P::S - 1, true>(sm, f, lt, true, tw, gload, gstore);
-    });
+    pass_tile<P, !FIRST>(sm, f, lt, c, g.Ns, tw, twA, twB, csign_in, csign_out);
     if constexpr (!FIRST) {
       fence_proxy_async_smem();
       __syncthreads();
@@ -106,15 +73,8 @@ __global__ void __launch_bounds__(P::THREADS, MINB)
       }
     } else {
       __syncthreads();
-      // pass 0: column c's outputs are contiguous at c L + r; lanes walk r
-      float2* go = out_first + (long long)b * g.N + (long long)c0 * L;
-      constexpr int PER = L * C / P::THREADS;
-      sfor<PER>([&](auto n_) {
-        constexpr int n = decltype(n_)::value;
-        const int e = threadIdx.x + n * P::THREADS;
-        const int r = e % L, cc = e / L;
-        __stcs(go + cc * L + r, sm[P::sidx(cc, r)]);
-      });
+      pass0_store<P>(sm, out_first + (long long)b * g.N + (long long)c0 * L,
+                     [](float2* q, float2 v) { __stcs(q, v); });
       __syncthreads();
     }
     if (threadIdx.x == 0 && t + 2 * (long long)gridDim.x < T) {

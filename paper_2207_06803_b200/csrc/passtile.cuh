@@ -1,0 +1,78 @@
+// passtile.cuh -- one tile of a large-N Stockham pass (product path).
+//
+// A pass of length L is one level of the paper's Eq. 2 applied at the
+// pass level (SURVEY App. A.2 with radix -> L):
+//   column c < N/L, Ns = product of the earlier pass lengths:
+//     v[r]  = a[c + r N/L]                                  (Pi folded into the column read)
+//     v[r] *= w_{Ns L}^{(c mod Ns) r}          (Ns > 1)      (D^{Ns L}_{Ns})
+//     v     = DFT_L v                                       (fused Stockham sub-stages, fused.cuh)
+//     b[(c div Ns) Ns L + (c mod Ns) + r Ns] = v[r]
+// A tile is 16 adjacent columns held in shared memory as the TMA 128-byte-swizzled
+// [L rows][16 columns] layout (LAY_TMA128).  pass_tile transforms it in place; both the
+// HBM multi-pass kernels (passes.cu) and the L2-resident kernel (l2pass.cu) call it, so
+// the two paths compute bit-identical results.
+#pragma once
+#include "colfft.cuh"
+
+namespace fftc {
+
+// DFT_L of the 16 columns of the tile, in place.  c = this thread's column (c0 + f);
+// the input twiddle w_{Ns L}^{(c mod Ns) i} is applied when TW (every pass but the first).
+template <class P, bool TW>
+__device__ __forceinline__ void pass_tile(float2* sm, int f, int lt, int c, int Ns,
+                                          const float2* __restrict__ tw, const float2* __restrict__ twA,
+                                          const float2* __restrict__ twB, float csign_in, float csign_out) {
+  static_assert(P::FPB == 16 && P::LAY == LAY_TMA128, "pass tiles are 16 columns, TMA 128B swizzle");
+  constexpr int L = P::N;
+  constexpr int R0 = P::R(0);
+  constexpr int NB0 = L / R0;                      // sub-stage 0: element i = j + r NB0
+  constexpr int NB2 = ilog2(highbit(R0 - 1)) + 1;  // step powers for r < R0
+  // input twiddle w_T^{m i}, T = Ns L, m = c mod Ns: base per butterfly, step powers per thread
+  const long long m = TW ? (long long)(c % Ns) : 0;
+  float2 sp[NB2];
+  if constexpr (TW) {
+    sp[0] = root_lookup(twA, twB, m * NB0);
+    sfor<NB2 - 1>([&](auto b_) {
+      constexpr int bb = decltype(b_)::value + 1;
+      sp[bb] = cmul(sp[bb - 1], sp[bb - 1]);
+    });
+  }
+  float2 base = make_float2(1.f, 0.f);
+  auto gload = [&](int i, int r) {
+    float2 v = sm[P::sidx(f, i)];
+    v.y *= csign_in;
+    if constexpr (TW) {
+      if (r == 0) base = root_lookup(twA, twB, m * i);
+      float2 w = base;
+      sfor<NB2>([&](auto b_) {
+        constexpr int bb = decltype(b_)::value;
+        if (r & (1 << bb)) w = cmul(w, sp[bb]);
+      });
+      v = cmul(v, w);
+    }
+    return v;
+  };
+  auto gstore = [&](int i, float2 v, int) { sm[P::sidx(f, i)] = make_float2(v.x, csign_out * v.y); };
+  // sub-stages of DFT_L in place on the tile (every stage reads all, syncs, writes)
+  sfor<P::S>([&](auto s_) {
+    constexpr int s = decltype(s_)::value;
+    stage<P, s, s == 0, s == P::S - 1, true>(sm, f, lt, true, tw, gload, gstore);
+  });
+}
+
+// First pass (Ns = 1): column c's L outputs are contiguous at c L + r; go = base + c0 L.
+// Lanes walk r (coalesced 8-byte stores through st(ptr, value)).  Caller syncs before.
+template <class P, class ST>
+__device__ __forceinline__ void pass0_store(const float2* sm, float2* __restrict__ go, ST&& st) {
+  constexpr int L = P::N, C = 16;
+  constexpr int PER = L * C / P::THREADS;
+  static_assert((L * C) % P::THREADS == 0, "tile must split evenly");
+  sfor<PER>([&](auto n_) {
+    constexpr int n = decltype(n_)::value;
+    const int e = threadIdx.x + n * P::THREADS;
+    const int r = e % L, cc = e / L;
+    st(go + cc * L + r, sm[P::sidx(cc, r)]);
+  });
+}
+
+}  // namespace fftc

@@ -4,12 +4,13 @@
 #include <stdint.h>
 
 #include "fourstep.h"
+#include "l2pass.h"
 #include "passes.h"
 #include "registry.h"
 
 namespace fftc {
 
-enum PlanKind : int { KIND_COPY = 0, KIND_FUSED = 1, KIND_GENERIC = 2, KIND_FOURSTEP = 3, KIND_DIST = 4, KIND_PASSES = 5 };
+enum PlanKind : int { KIND_COPY = 0, KIND_FUSED = 1, KIND_GENERIC = 2, KIND_FOURSTEP = 3, KIND_DIST = 4, KIND_PASSES = 5, KIND_L2 = 6 };
 
 struct DistState;  // dist.cu
 
@@ -43,6 +44,8 @@ struct fftc_plan {
   float2* d_work = nullptr;    // N*batch complex
   // multi-pass TMA path (power-of-two N > 4096)
   fftc::PassPlanData pp;
+  // L2-resident multi-pass path (power-of-two N in 2^13..2^21)
+  fftc::L2PlanData l2;
   // host-buffer execution
   fftc::HostStage* hs = nullptr;
   // distributed six-step

@@ -74,7 +74,7 @@ def test_small_batches(N, batch, sign):
 
 @pytest.mark.parametrize("N", [1 << 16, 1 << 20])
 @pytest.mark.parametrize("sign", [-1, 1])
-@pytest.mark.parametrize("large", ["passes", "fourstep"])
+@pytest.mark.parametrize("large", ["l2", "passes", "fourstep"])
 def test_fourstep_small_batch(N, sign, large, monkeypatch):
     monkeypatch.setenv("FFTC_LARGE", large)
     x = synth.normal_c64(N, 3, seed=N)
@@ -86,7 +86,8 @@ def test_fourstep_small_batch(N, sign, large, monkeypatch):
 
 @pytest.mark.parametrize("n", list(range(13, 25)))
 def test_multipass_all_pow2(n):
-    """Every power of two 2^13..2^24 on the multi-pass TMA path (2-3 passes), both signs, odd batch."""
+    """Every power of two 2^13..2^24 on the default large-N path (HBM multi-pass), both
+    signs, odd batch."""
     N = 1 << n
     batch = max(1, (1 << 22) // N) | 1
     x = synth.uniform_c64(N, batch, seed=n)
@@ -94,6 +95,43 @@ def test_multipass_all_pow2(n):
         y = gpu_fft(x, sign)
         idx = sample_idx(batch, n_rand=4)
         check(y[idx], x[idx], sign)
+
+
+# ---------------------------------------------------------------- L2-resident multi-pass path
+L2_CASES = [(13, 83), (14, 37), (15, 21), (16, 11), (17, 7), (18, 5), (19, 4), (20, 3), (21, 2)]
+
+
+@pytest.mark.parametrize("n,batch", L2_CASES)
+def test_l2_path_many_chunks(n, batch, monkeypatch):
+    """L2-resident path with 1 MiB chunks: many chunks, ragged last chunk, the ring of
+    workspace slots wraps several times; both signs against the oracle."""
+    monkeypatch.setenv("FFTC_L2_CHUNK_MB", "1")
+    monkeypatch.setenv("FFTC_LARGE", "l2")
+    N = 1 << n
+    x = synth.uniform_c64(N, batch, seed=100 + n)
+    with fftc.Plan(N, batch, -1) as p:
+        assert "kind=l2" in p.describe(), p.describe()
+    idx = np.array(sorted({0, 1, batch // 2, batch - 2, batch - 1}), dtype=np.int64)
+    for sign in (-1, 1):
+        y = gpu_fft(x, sign)
+        check(y[idx], x[idx], sign)
+
+
+@pytest.mark.parametrize("n", [13, 16, 17, 20])
+def test_l2_matches_hbm_multipass(n, monkeypatch):
+    """The L2-resident kernel runs the same pass tiles (passtile.cuh, same radices and
+    twiddle tables) as the HBM multi-pass kernels: the two agree to fp32 rounding
+    (not bitwise: the compiler may contract differently inside the two kernels)."""
+    N = 1 << n
+    batch = max(2, (1 << 22) // N) + 1
+    x = synth.uniform_c64(N, batch, seed=n)
+    monkeypatch.setenv("FFTC_L2_CHUNK_MB", "2")
+    monkeypatch.setenv("FFTC_LARGE", "l2")
+    y_l2 = gpu_fft(x, -1)
+    monkeypatch.setenv("FFTC_LARGE", "passes")
+    y_hbm = gpu_fft(x, -1)
+    d = oracle.rel_l2(y_l2, y_hbm.astype(np.complex128))
+    assert d.max() <= 2e-7, float(d.max())
 
 
 @pytest.mark.parametrize("N", POW2 + MIXED)
@@ -225,9 +263,9 @@ def test_boundary_errors():
 
 
 def test_describe_and_launches():
-    for N, kind, launches in [(64, "fused", 1), (4096, "fused", 1), (48, "generic", 1), (1 << 20, "fourstep", 2),
-                              (1 << 24, "passes", 3), (1 << 13, "passes", 2),
-                              (1 << 16, "passes", 2)]:
+    for N, kind, launches in [(64, "fused", 1), (4096, "fused", 1), (48, "generic", 1), (1 << 20, "passes", 3),
+                              (1 << 24, "passes", 3), (1 << 13, "passes", 2), (1 << 16, "passes", 2),
+                              (1 << 22, "passes", 3)]:
         with fftc.Plan(N, 2, -1) as p:
             assert ("kind=" + kind) in p.describe()
             assert p.launches() == launches
@@ -243,6 +281,21 @@ def test_execute_host_matches_device():
     assert np.array_equal(out, y)  # same kernels, same result bit for bit
     idx = sample_idx(batch)
     check(out[idx], x[idx], -1)
+
+
+def test_execute_host_matches_device_l2(monkeypatch):
+    """Host-staged execution of an L2-path plan (each staging slot owns its ring + counters)."""
+    monkeypatch.setenv("FFTC_LARGE", "l2")
+    N, batch = 1 << 16, 150
+    x = synth.uniform_c64(N, batch, seed=4)
+    out = np.empty_like(x)
+    with fftc.Plan(N, batch, 1) as p:
+        assert "kind=l2" in p.describe()
+        p.execute_host(x, out)
+    y = gpu_fft(x, 1)
+    assert np.array_equal(out, y)
+    idx = np.array([0, 63, 64, 149])
+    check(out[idx], x[idx], 1)
 
 
 def test_determinism_bitwise():
