@@ -59,9 +59,11 @@ struct Radices {
 //   LAY_ODD  : f*SS + i, SS odd (F_FAST, other N).
 //   LAY_INTER: swzc(i)*FPB + f (interleaved columns, F_FAST with FPB < 16: a phase
 //              holds FPB columns x 16/FPB consecutive butterflies).
+//   LAY_TMA64: i*8 + (((f >> 1) ^ ((i >> 1) & 3)) << 1 | (f & 1)) -- the TMA 64-byte swizzle of a
+//              [row i][8 columns] complex64 tile (512-byte aligned), FPB = 8.
 //   LAY_TMA128: i*16 + (((f >> 1) ^ (i & 7)) << 1 | (f & 1)) -- the TMA 128-byte swizzle of a
 //              [row i][16 columns] complex64 tile (1024-byte aligned), FPB = 16.
-enum Layout : int { LAY_AUTO = -1, LAY_SWZ = 0, LAY_FXOR = 1, LAY_ODD = 2, LAY_INTER = 3, LAY_TMA128 = 4 };
+enum Layout : int { LAY_AUTO = -1, LAY_SWZ = 0, LAY_FXOR = 1, LAY_ODD = 2, LAY_INTER = 3, LAY_TMA128 = 4, LAY_TMA64 = 5 };
 
 constexpr int ilog2(int n) {
   int l = 0;
@@ -98,6 +100,7 @@ struct Sched {
   FFTC_HD static int sidx(int f, int i) {
     if constexpr (LAY == LAY_FXOR) return f * SS + (i ^ gf(f));
     else if constexpr (LAY == LAY_TMA128) return i * 16 + ((((f >> 1) ^ (i & 7)) << 1) | (f & 1));
+    else if constexpr (LAY == LAY_TMA64) return i * 8 + ((((f >> 1) ^ ((i >> 1) & 3)) << 1) | (f & 1));
     else if constexpr (LAY == LAY_INTER) return (i ^ ((i >> ISHIFT) & IMASK)) * FPB + f;
     else return f * SS + swz(i);
   }

@@ -8,10 +8,11 @@
 //     v[r] *= w_{Ns L}^{(c mod Ns) r}          (s > 0)       (D^{Ns L}_{Ns})
 //     v     = DFT_{L_s} v                                   (a fused Stockham pass, fused.cuh)
 //     b[(c div Ns) Ns L + (c mod Ns) + r Ns] = v[r]         (natural order after the last pass)
-// A CTA owns 16 adjacent columns (one 128-byte segment per row).  The [L rows][16 cols]
-// tile is fetched by ONE 3-D TMA tensor load (cp.async.bulk.tensor, 128B-swizzled shared
-// layout, completion on an mbarrier), transformed in place, and -- for s > 0 -- written
-// back by ONE 4-D TMA tensor store (the autosort write is a [L][16] box of a
+// A CTA owns C = 16 adjacent columns (one 128-byte segment per row; C = 8, 64-byte rows,
+// for L = 512 / 1024).  The [L rows][C cols] tile is fetched by ONE 3-D TMA tensor load
+// (cp.async.bulk.tensor, 128B/64B-swizzled shared layout, completion on an mbarrier),
+// transformed in place, and -- for s > 0 -- written back by ONE 4-D TMA tensor store
+// (the autosort write is a [L][C] box of a
 // (Ns, L, NB/Ns, batch) view).  Pass 0 (Ns = 1) writes each column's L outputs
 // contiguously, via coalesced 8-byte stores.  CTAs are persistent and double-buffered:
 // the tile after next streams in while the current one is computed.
@@ -27,13 +28,13 @@ namespace fftc {
 
 namespace {
 
-template <class P, bool FIRST, int MINB>
+template <class P, bool FIRST, int MINB, int NBUF>
 __global__ void __launch_bounds__(P::THREADS, MINB)
     k_pass(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout,
            float2* __restrict__ out_first, const float2* __restrict__ tw, const float2* __restrict__ twA,
            const float2* __restrict__ twB, PassGeom g, float csign_in, float csign_out) {
-  static_assert(P::FPB == 16 && P::LAY == LAY_TMA128, "pass tiles are 16 columns, TMA 128B swizzle");
-  constexpr int L = P::N, C = 16;
+  static_assert(NBUF == 1 || NBUF == 2, "one or two tile buffers");
+  constexpr int L = P::N, C = P::FPB;
   constexpr uint32_t TILE_BYTES = (uint32_t)L * C * 8u;
   extern __shared__ __align__(1024) unsigned char smraw[];
   float2* buf0 = reinterpret_cast<float2*>(smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u));
@@ -42,10 +43,14 @@ __global__ void __launch_bounds__(P::THREADS, MINB)
   P::thread_coords(threadIdx.x, f, lt);
   const long long T = g.tiles_total;
   const int tpb = g.tiles_per_batch;
+  constexpr int BOX = L < 256 ? L : 256;  // TMA boxes are at most 256 rows
   auto issue = [&](long long t, int k) {
     const int b = (int)(t / tpb), c0 = (int)(t % tpb) * C;
     mbar_arrive_expect_tx(&full[k], TILE_BYTES);
-    tma_load_3d(buf0 + k * L * C, &tin, c0, 0, b, &full[k]);
+    sfor<L / BOX>([&](auto h_) {
+      constexpr int h = decltype(h_)::value;
+      tma_load_3d(buf0 + k * L * C + h * BOX * C, &tin, c0, h * BOX, b, &full[k]);
+    });
   };
   if (threadIdx.x == 0) {
     mbar_init(&full[0], 1);
@@ -54,21 +59,24 @@ __global__ void __launch_bounds__(P::THREADS, MINB)
   __syncthreads();
   if (threadIdx.x == 0) {
     if (blockIdx.x < T) issue(blockIdx.x, 0);
-    if (blockIdx.x + gridDim.x < T) issue(blockIdx.x + gridDim.x, 1);
+    if (NBUF == 2 && blockIdx.x + gridDim.x < T) issue(blockIdx.x + gridDim.x, 1);
   }
   int it = 0;
   for (long long t = blockIdx.x; t < T; t += gridDim.x, ++it) {
-    const int k = it & 1;
+    const int k = NBUF == 2 ? (it & 1) : 0;
     float2* sm = buf0 + k * L * C;
     const int b = (int)(t / tpb), c0 = (int)(t % tpb) * C;
     const int c = c0 + f;
-    mbar_wait(&full[k], (it >> 1) & 1);
+    mbar_wait(&full[k], NBUF == 2 ? ((it >> 1) & 1) : (it & 1));
     pass_tile<P, !FIRST>(sm, f, lt, c, g.Ns, tw, twA, twB, csign_in, csign_out);
     if constexpr (!FIRST) {
       fence_proxy_async_smem();
       __syncthreads();
       if (threadIdx.x == 0) {
-        tma_store_4d(&tout, sm, c0 % g.Ns, 0, c0 / g.Ns, b);
+        sfor<L / BOX>([&](auto h_) {
+          constexpr int h = decltype(h_)::value;
+          tma_store_4d(&tout, sm + h * BOX * C, c0 % g.Ns, h * BOX, c0 / g.Ns, b);
+        });
         bulk_commit();
       }
     } else {
@@ -77,22 +85,22 @@ __global__ void __launch_bounds__(P::THREADS, MINB)
                      [](float2* q, float2 v) { __stcs(q, v); });
       __syncthreads();
     }
-    if (threadIdx.x == 0 && t + 2 * (long long)gridDim.x < T) {
+    if (threadIdx.x == 0 && t + NBUF * (long long)gridDim.x < T) {
       if constexpr (!FIRST) bulk_wait_read0();  // the store has finished reading this buffer
-      issue(t + 2 * (long long)gridDim.x, k);
+      issue(t + NBUF * (long long)gridDim.x, k);
     }
   }
   if constexpr (!FIRST)
     if (threadIdx.x == 0) bulk_wait0();
 }
 
-template <class P, int MINB>
+template <class P, int MINB, int NBUF>
 cudaError_t launch_pass(bool first, const CUtensorMap& tin, const CUtensorMap& tout, float2* out_first,
                         const float2* tw, const float2* twA, const float2* twB, const PassGeom& g, int conj_in,
                         int conj_out, cudaStream_t st) {
-  constexpr size_t smem = (size_t)2 * P::N * 16 * sizeof(float2) + 1024;
+  constexpr size_t smem = (size_t)NBUF * P::N * P::FPB * sizeof(float2) + 1024;
   static int grid_max[2] = {0, 0};
-  auto kern = first ? k_pass<P, true, MINB> : k_pass<P, false, MINB>;
+  auto kern = first ? k_pass<P, true, MINB, NBUF> : k_pass<P, false, MINB, NBUF>;
   int& gm = grid_max[first ? 1 : 0];
   if (!gm) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -113,24 +121,41 @@ cudaError_t launch_pass(bool first, const CUtensorMap& tin, const CUtensorMap& t
 
 }  // namespace
 
-#define FFTC_PASS(NAME, L, RAD, TPF, MINB, ...) \
-  {L, RAD::S, {__VA_ARGS__}, TPF, &launch_pass<Sched<L, RAD, TPF, 16, F_FAST, 0, LAY_TMA128>, MINB>, NAME}
+// C = 16 columns (128-byte rows, TMA 128B swizzle) for L <= 256; C = 8 (64-byte rows, 64B
+// swizzle) for L = 512 / 1024 so a tile stays <= 64 KB.
+#define FFTC_PASS(NAME, L, RAD, TPF, MINB, NBUF, ...)                                                    \
+  {L, RAD::S, {__VA_ARGS__}, TPF, 16, &launch_pass<Sched<L, RAD, TPF, 16, F_FAST, 0, LAY_TMA128>, MINB, NBUF>, \
+   NAME}
+#define FFTC_PASS8(NAME, L, RAD, TPF, MINB, NBUF, ...)                                                  \
+  {L, RAD::S, {__VA_ARGS__}, TPF, 8, &launch_pass<Sched<L, RAD, TPF, 8, F_FAST, 0, LAY_TMA64>, MINB, NBUF>, \
+   NAME}
 
 using PRad_4x4 = Radices<4, 4>;
 using PRad_8x4 = Radices<8, 4>;
 using PRad_8x8 = Radices<8, 8>;
 using PRad_16x8 = Radices<16, 8>;
 using PRad_16x16 = Radices<16, 16>;
+using PRad_32x16 = Radices<32, 16>;
+using PRad_16x32 = Radices<16, 32>;
+using PRad_32x32 = Radices<32, 32>;
 
+// First entry per length = default; FFTC_PASS=<name> pins a candidate (tuning).
 static const PassEntry kPasses[] = {
-    FFTC_PASS("p16_r4x4", 16, PRad_4x4, 4, 8, 4, 4),
-    FFTC_PASS("p32_r8x4", 32, PRad_8x4, 4, 8, 8, 4),
-    FFTC_PASS("p64_r8x8", 64, PRad_8x8, 8, 6, 8, 8),
-    FFTC_PASS("p128_r16x8", 128, PRad_16x8, 16, 3, 16, 8),
-    FFTC_PASS("p256_r16x16", 256, PRad_16x16, 16, 3, 16, 16),
+    FFTC_PASS("p16_r4x4", 16, PRad_4x4, 4, 8, 2, 4, 4),
+    FFTC_PASS("p32_r8x4", 32, PRad_8x4, 4, 8, 2, 8, 4),
+    FFTC_PASS("p64_r8x8", 64, PRad_8x8, 8, 6, 2, 8, 8),
+    FFTC_PASS("p128_r16x8", 128, PRad_16x8, 16, 3, 2, 16, 8),
+    FFTC_PASS("p256_r16x16", 256, PRad_16x16, 16, 3, 2, 16, 16),
+    FFTC_PASS8("p512_r16x32_c8t32", 512, PRad_16x32, 32, 2, 2, 16, 32),
+    FFTC_PASS8("p512_r32x16_c8", 512, PRad_32x16, 16, 3, 2, 32, 16),
+    FFTC_PASS8("p1024_r32x32_c8b2", 1024, PRad_32x32, 32, 1, 2, 32, 32),
+    FFTC_PASS8("p1024_r32x32_c8b1", 1024, PRad_32x32, 32, 3, 1, 32, 32),
 };
 
 const PassEntry* find_pass(int L) {
+  if (const char* want = getenv("FFTC_PASS"))
+    for (const auto& e : kPasses)
+      if (e.L == L && strcmp(e.name, want) == 0) return &e;
   for (const auto& e : kPasses)
     if (e.L == L) return &e;
   return nullptr;
@@ -153,46 +178,53 @@ static encode_fn get_encode() {
   return fn;
 }
 
-// in: a [batch][L rows][NB cols] view, box [16 cols][L rows]
-static bool map_in(CUtensorMap* m, const void* base, long long N, int L, long long batch) {
+// in: a [batch][L rows][NB cols] view, box [C cols][min(L, 256) rows] (the TMA box limit)
+static bool map_in(CUtensorMap* m, const void* base, long long N, int L, int C, long long batch) {
   encode_fn enc = get_encode();
   if (!enc) return false;
   const long long NB = N / L;
   cuuint64_t dims[3] = {(cuuint64_t)NB, (cuuint64_t)L, (cuuint64_t)batch};
   cuuint64_t strides[2] = {(cuuint64_t)NB * 8, (cuuint64_t)N * 8};
-  cuuint32_t box[3] = {16, (cuuint32_t)L, 1};
+  cuuint32_t box[3] = {(cuuint32_t)C, (cuuint32_t)(L < 256 ? L : 256), 1};
   cuuint32_t es[3] = {1, 1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_INT64, 3, const_cast<void*>(base), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, C == 16 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
-// out (autosort write): a [batch][NB/Ns][L][Ns] view, box [16][L][1][1]
-static bool map_out(CUtensorMap* m, void* base, long long N, int L, long long Ns, long long batch) {
+// out (autosort write): a [batch][NB/Ns][L][Ns] view, box [C][min(L, 256)][1][1]
+static bool map_out(CUtensorMap* m, void* base, long long N, int L, int C, long long Ns, long long batch) {
   encode_fn enc = get_encode();
   if (!enc) return false;
   const long long NB = N / L;
   cuuint64_t dims[4] = {(cuuint64_t)Ns, (cuuint64_t)L, (cuuint64_t)(NB / Ns), (cuuint64_t)batch};
   cuuint64_t strides[3] = {(cuuint64_t)Ns * 8, (cuuint64_t)Ns * L * 8, (cuuint64_t)N * 8};
-  cuuint32_t box[4] = {16, (cuuint32_t)L, 1, 1};
+  cuuint32_t box[4] = {(cuuint32_t)C, (cuuint32_t)(L < 256 ? L : 256), 1, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_INT64, 4, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             C == 16 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 bool passes_available() { return get_encode() != nullptr; }
 
-// Split N (power of two, 2^9 .. 2^32) into p = ceil(log2 N / 8) pass lengths in [16, 256],
+// Split N (power of two, 2^9 .. 2^48) into p passes: p = ceil(log2 N / 8) with lengths in
+// [16, 256], except that 2^17 .. 2^20 take two passes of up to 1024 (8-column tiles) --
+// one HBM round trip fewer (env FFTC_PASS_MAXLOG=8 restores three passes).  Lengths are
 // as equal as possible, larger first.
 int pass_split(long long N, int* Ls, int max) {
   if (N < 512 || (N & (N - 1))) return -1;
   int n = 0;
   while ((1LL << n) < N) ++n;
-  const int p = (n + 7) / 8;
+  int maxlog = 10;
+  if (const char* m = getenv("FFTC_PASS_MAXLOG")) maxlog = atoi(m);
+  if (maxlog < 8) maxlog = 8;
+  if (maxlog > 10) maxlog = 10;
+  int p = (n + 7) / 8;
+  if (p == 3 && n <= 2 * maxlog) p = 2;
   if (p > max) return -1;
   for (int s = 0; s < p; ++s) {
     const int e = n / p + (s < n % p ? 1 : 0);
-    if (e < 4 || e > 8) return -1;
+    if (e < 4 || e > maxlog) return -1;
     Ls[s] = 1 << e;
   }
   return p;
@@ -209,11 +241,11 @@ cudaError_t passes_execute(const PassPlanData& pp, const float2* in, float2* out
     const PassEntry* e = pp.e[s];
     const int L = e->L;
     CUtensorMap tin, tout;
-    if (!map_in(&tin, src, pp.N, L, batch)) return cudaErrorInvalidValue;
-    if (s > 0 && !map_out(&tout, dst, pp.N, L, Ns, batch)) return cudaErrorInvalidValue;
+    if (!map_in(&tin, src, pp.N, L, e->cols, batch)) return cudaErrorInvalidValue;
+    if (s > 0 && !map_out(&tout, dst, pp.N, L, e->cols, Ns, batch)) return cudaErrorInvalidValue;
     if (s == 0) memset(&tout, 0, sizeof(tout));
     PassGeom g{};
-    g.tiles_per_batch = (int)(pp.N / L / 16);
+    g.tiles_per_batch = (int)(pp.N / L / e->cols);
     g.tiles_total = batch * g.tiles_per_batch;
     g.Ns = (int)Ns;
     g.N = pp.N;

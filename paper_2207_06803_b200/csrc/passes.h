@@ -8,7 +8,7 @@ namespace fftc {
 
 struct PassGeom {
   long long tiles_total;  // batch * tiles_per_batch
-  int tiles_per_batch;    // (N / L) / 16
+  int tiles_per_batch;    // (N / L) / cols
   int Ns;                 // Stockham Ns of this pass (product of earlier pass lengths)
   long long N;
   int tw;                 // apply the input twiddle w_{Ns L}^{(c mod Ns) r}
@@ -23,6 +23,7 @@ struct PassEntry {
   int S;
   int R[8];
   int tpf;
+  int cols;  // columns per tile (16: 128-byte rows; 8: 64-byte rows)
   pass_launch_fn launch;
   const char* name;
 };

@@ -7,8 +7,8 @@
 //     v[r] *= w_{Ns L}^{(c mod Ns) r}          (Ns > 1)      (D^{Ns L}_{Ns})
 //     v     = DFT_L v                                       (fused Stockham sub-stages, fused.cuh)
 //     b[(c div Ns) Ns L + (c mod Ns) + r Ns] = v[r]
-// A tile is 16 adjacent columns held in shared memory as the TMA 128-byte-swizzled
-// [L rows][16 columns] layout (LAY_TMA128).  pass_tile transforms it in place; both the
+// A tile is C = 16 (or 8) adjacent columns held in shared memory as the TMA 128-byte
+// (64-byte) swizzled [L rows][C columns] layout (LAY_TMA128 / LAY_TMA64).  pass_tile transforms it in place; both the
 // HBM multi-pass kernels (passes.cu) and the L2-resident kernel (l2pass.cu) call it, so
 // the two paths compute bit-identical results.
 #pragma once
@@ -16,13 +16,14 @@
 
 namespace fftc {
 
-// DFT_L of the 16 columns of the tile, in place.  c = this thread's column (c0 + f);
+// DFT_L of the C columns of the tile, in place.  c = this thread's column (c0 + f);
 // the input twiddle w_{Ns L}^{(c mod Ns) i} is applied when TW (every pass but the first).
 template <class P, bool TW>
 __device__ __forceinline__ void pass_tile(float2* sm, int f, int lt, int c, int Ns,
                                           const float2* __restrict__ tw, const float2* __restrict__ twA,
                                           const float2* __restrict__ twB, float csign_in, float csign_out) {
-  static_assert(P::FPB == 16 && P::LAY == LAY_TMA128, "pass tiles are 16 columns, TMA 128B swizzle");
+  static_assert((P::FPB == 16 && P::LAY == LAY_TMA128) || (P::FPB == 8 && P::LAY == LAY_TMA64),
+                "pass tiles: 16 columns with the TMA 128B swizzle or 8 columns with the 64B swizzle");
   constexpr int L = P::N;
   constexpr int R0 = P::R(0);
   constexpr int NB0 = L / R0;                      // sub-stage 0: element i = j + r NB0
@@ -64,7 +65,7 @@ __device__ __forceinline__ void pass_tile(float2* sm, int f, int lt, int c, int 
 // Lanes walk r (coalesced 8-byte stores through st(ptr, value)).  Caller syncs before.
 template <class P, class ST>
 __device__ __forceinline__ void pass0_store(const float2* sm, float2* __restrict__ go, ST&& st) {
-  constexpr int L = P::N, C = 16;
+  constexpr int L = P::N, C = P::FPB;
   constexpr int PER = L * C / P::THREADS;
   static_assert((L * C) % P::THREADS == 0, "tile must split evenly");
   sfor<PER>([&](auto n_) {

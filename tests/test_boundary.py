@@ -90,7 +90,10 @@ def test_planner_passes():
     for n in range(9, 41):
         Ls = fftc.fftc_plan_passes(1 << n)
         assert Ls is not None and math.prod(Ls) == 1 << n
-        assert len(Ls) == (n + 7) // 8 and all(16 <= L <= 256 for L in Ls)
+        want = 2 if 17 <= n <= 20 else (n + 7) // 8  # 2^17..2^20: two passes of <= 1024
+        assert len(Ls) == want, (n, Ls)
+        assert all(16 <= L <= (1024 if want == 2 else 256) for L in Ls)
+        assert Ls == sorted(Ls, reverse=True) and max(Ls) <= 2 * min(Ls)
     assert fftc.fftc_plan_passes(3 * 4096) is None
     assert fftc.fftc_plan_passes(256) is None
 

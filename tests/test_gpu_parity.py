@@ -97,6 +97,21 @@ def test_multipass_all_pow2(n):
         check(y[idx], x[idx], sign)
 
 
+@pytest.mark.parametrize("n,name", [(17, "p512_r32x16_c8"), (18, "p512_r32x16_c8"), (18, "p512_r16x32_c8t32"),
+                                    (19, "p1024_r32x32_c8b1"), (20, "p1024_r32x32_c8b1"),
+                                    (20, "p1024_r32x32_c8b2")])
+def test_every_pass_candidate(n, name, monkeypatch):
+    """Each compiled 8-column pass kernel (L = 512 / 1024, TMA boxes split at 256 rows)."""
+    monkeypatch.setenv("FFTC_PASS", name)
+    N = 1 << n
+    batch = 3
+    x = synth.uniform_c64(N, batch, seed=n)
+    with fftc.Plan(N, batch, -1) as p:
+        assert name in p.describe(), p.describe()
+    for sign in (-1, 1):
+        check(gpu_fft(x, sign), x, sign)
+
+
 # ---------------------------------------------------------------- L2-resident multi-pass path
 L2_CASES = [(13, 83), (14, 37), (15, 21), (16, 11), (17, 7), (18, 5), (19, 4), (20, 3), (21, 2)]
 
@@ -129,6 +144,7 @@ def test_l2_matches_hbm_multipass(n, monkeypatch):
     monkeypatch.setenv("FFTC_LARGE", "l2")
     y_l2 = gpu_fft(x, -1)
     monkeypatch.setenv("FFTC_LARGE", "passes")
+    monkeypatch.setenv("FFTC_PASS_MAXLOG", "8")  # the same pass lengths as the L2 split
     y_hbm = gpu_fft(x, -1)
     d = oracle.rel_l2(y_l2, y_hbm.astype(np.complex128))
     assert d.max() <= 2e-7, float(d.max())
@@ -263,7 +279,7 @@ def test_boundary_errors():
 
 
 def test_describe_and_launches():
-    for N, kind, launches in [(64, "fused", 1), (4096, "fused", 1), (48, "generic", 1), (1 << 20, "passes", 3),
+    for N, kind, launches in [(64, "fused", 1), (4096, "fused", 1), (48, "generic", 1), (1 << 20, "passes", 2),
                               (1 << 24, "passes", 3), (1 << 13, "passes", 2), (1 << 16, "passes", 2),
                               (1 << 22, "passes", 3)]:
         with fftc.Plan(N, 2, -1) as p:

@@ -1,5 +1,8 @@
 cd $GRAFT_REPO_ROOT
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "l2 or multipass or fourstep_small or execute_host or describe or config4" 2>&1 | tail -3
-for n in 13 14 15 16 17 18 19 20 21 22 23 24; do for m in passes fourstep; do FFTC_LARGE=$m timeout 100 python tools/l2sweep.py one $n $(( (1<<28) >> n )) | cut -c1-120; done; done
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_pass -c 2 -o gpurun_out/prof_pass16 python tools/l2sweep.py one 16 1024 > gpurun_out/ncu_p.log 2>&1
-tail -1 gpurun_out/ncu_p.log
+timeout 1500 python -m pytest tests -x -q -m gpu 2>&1 | tail -3
+python bench.py --workload c4 --no-e2e --no-cpu 2>&1 | tail -1 > gpurun_out/bench_c4.json; head -c 300 gpurun_out/bench_c4.json; echo
+python - <<'PY'
+import json
+d=json.loads(open('gpurun_out/bench_c4.json').read())
+for j in d['per_job']: print(j)
+PY
