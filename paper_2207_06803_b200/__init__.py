@@ -9,7 +9,7 @@ Functions keep the C names (``fftc_plan_create``, ``fftc_execute``,
 ``fftc_execute_host``, ``fftc_plan_destroy``, ``fftc_last_error``,
 ``fftc_status_string``, ``fftc_plan_describe``, ``fftc_plan_launches``,
 ``fftc_factorize``, ``fftc_plan_split``, ``fftc_dist_get_unique_id``,
-``fftc_dist_plan_create``, ``fftc_dist_split``, ``fftc_candidates``, ``fftc_plan_passes``); :class:`Plan` is a convenience wrapper that owns a
+``fftc_dist_plan_create``, ``fftc_dist_split``, ``fftc_candidates``, ``fftc_plan_passes``, ``fftc_plan_gpasses``); :class:`Plan` is a convenience wrapper that owns a
 plan handle and takes contiguous ``torch.complex64`` CUDA tensors.
 """
 from __future__ import annotations
@@ -65,6 +65,7 @@ def load(path: str = LIB_PATH):
         "fftc_dist_split": ([i64, i32, ctypes.POINTER(ctypes.c_int64)], i32),
         "fftc_candidates": ([i64, ctypes.POINTER(ctypes.c_char_p), i32], i32),
         "fftc_plan_passes": ([i64, ctypes.POINTER(ctypes.c_int), i32], i32),
+        "fftc_plan_gpasses": ([i64, ctypes.POINTER(ctypes.c_int), i32], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -124,6 +125,12 @@ def fftc_candidates(N: int):
 def fftc_plan_passes(N: int):
     arr = (ctypes.c_int * 8)()
     p = load().fftc_plan_passes(N, arr, 8)
+    return None if p < 0 else [arr[i] for i in range(p)]
+
+
+def fftc_plan_gpasses(N: int):
+    arr = (ctypes.c_int * 8)()
+    p = load().fftc_plan_gpasses(N, arr, 8)
     return None if p < 0 else [arr[i] for i in range(p)]
 
 

@@ -82,6 +82,8 @@ cudaError_t exec_local(const fftc_plan* p, const float2* in, float2* out, long l
       return passes_execute(p->pp, in, out, work, batch, conj, st);
     case KIND_L2:
       return l2_execute(p->l2, in, out, work, batch, conj, st);
+    case KIND_GPASS:
+      return gpass_execute(p->gp, in, out, work, batch, conj, st);
     case KIND_FOURSTEP: {
       const ColGeom g = fourstep_cols_geom(p->ce, p->N, p->K);
       cudaError_t e = p->ce->launch(in, work, p->d_tw, p->d_twA, p->d_twB, g, batch, conj, 0, st);
@@ -110,6 +112,7 @@ static void free_plan(fftc_plan* p) {
   cudaFree(p->d_twA);
   cudaFree(p->d_twB);
   cudaFree(p->d_work);
+  for (int i = 0; i < 3 * kMaxGPasses; ++i) cudaFree(p->gp_tables[i]);
   for (int s = 0; s < kMaxL2Passes; ++s) {
     cudaFree(p->l2.tw[s]);
     cudaFree(p->l2.twA[s]);
@@ -233,6 +236,7 @@ fftc_plan* fftc_plan_create(int64_t N, int64_t batch, int sign) {
   bool use_passes = np > 0 && passes_available();
   if (large && strcmp(large, "fourstep") == 0) use_passes = false;
   if (large && strcmp(large, "passes") == 0 && np > 0 && passes_available()) use_passes = true;
+  if (large && strcmp(large, "gpass") == 0) use_passes = false;
   if (use_passes) {
     p->kind = KIND_PASSES;
     p->pp.N = N;
@@ -249,6 +253,42 @@ fftc_plan* fftc_plan_create(int64_t N, int64_t batch, int sign) {
       Ns = T;
     }
     if (err == cudaSuccess && batch > 0 && np > 1) err = cudaMalloc(&p->d_work, (size_t)(N * batch) * sizeof(float2));
+    if (err != cudaSuccess) return fail(p, from_cuda(err));
+    return p;
+  }
+  // any other 7-smooth N (and FFTC_LARGE=gpass): runtime-schedule multi-pass kernels
+  const bool force_gpass = large && strcmp(large, "gpass") == 0;
+  if (np < 0 || force_gpass) {
+    int Lg[kMaxGPasses];
+    const int pg = gpass_split(N, Lg, kMaxGPasses);
+    if (pg < 0) return fail(p, FFTC_ERROR_UNSUPPORTED_SIZE);
+    p->kind = KIND_GPASS;
+    p->gp.N = N;
+    p->gp.p = pg;
+    int64_t Ns = 1;
+    for (int s = 0; s < pg && err == cudaSuccess; ++s) {
+      GPassStage& g = p->gp.st[s];
+      g.L = Lg[s];
+      g.Ns = (int)Ns;
+      g.S = generic_radices(Lg[s], g.R, kMaxStages);
+      if (g.S < 1) return fail(p, FFTC_ERROR_UNSUPPORTED_SIZE);
+      const int64_t T = Ns * Lg[s];
+      float2* t0 = upload_stage_table(Lg[s], g.R, g.S, &err);
+      p->gp_tables[3 * s] = t0;
+      g.tw = t0;
+      if (err == cudaSuccess) {
+        float2* t1 = upload_root_table(T, T < 4096 ? T : 4096, 1, &err);
+        p->gp_tables[3 * s + 1] = t1;
+        g.twA = t1;
+      }
+      if (err == cudaSuccess) {
+        float2* t2 = upload_root_table(T, (T + 4095) / 4096, 4096, &err);
+        p->gp_tables[3 * s + 2] = t2;
+        g.twB = t2;
+      }
+      Ns = T;
+    }
+    if (err == cudaSuccess && batch > 0 && pg > 1) err = cudaMalloc(&p->d_work, (size_t)(N * batch) * sizeof(float2));
     if (err != cudaSuccess) return fail(p, from_cuda(err));
     return p;
   }
@@ -304,7 +344,7 @@ fftc_status fftc_execute_host(fftc_plan* p, const void* host_in, void* host_out)
     for (int i = 0; i < HostStage::kDepth && e == cudaSuccess; ++i) {
       e = cudaMalloc(&hs->d_in[i], (size_t)(chunk * tbytes));
       if (e == cudaSuccess) e = cudaMalloc(&hs->d_out[i], (size_t)(chunk * tbytes));
-      if (e == cudaSuccess && (p->kind == KIND_FOURSTEP || p->kind == KIND_PASSES))
+      if (e == cudaSuccess && (p->kind == KIND_FOURSTEP || p->kind == KIND_PASSES || p->kind == KIND_GPASS))
         e = cudaMalloc(&hs->d_work[i], (size_t)(chunk * tbytes));
       if (e == cudaSuccess && p->kind == KIND_L2) e = cudaMalloc(&hs->d_work[i], l2_work_bytes(p->l2, chunk));
       if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&hs->st[i], cudaStreamNonBlocking);
@@ -357,6 +397,7 @@ int fftc_plan_launches(const fftc_plan* p) {
     case KIND_FOURSTEP: return p->batch > 0 ? 2 : 0;
     case KIND_PASSES: return p->batch > 0 ? p->pp.p : 0;
     case KIND_L2: return p->batch > 0 ? 1 : 0;
+    case KIND_GPASS: return p->batch > 0 ? p->gp.p : 0;
     case KIND_DIST: return dist_launches(p->dist);
   }
   return -1;
@@ -398,6 +439,17 @@ int fftc_plan_describe(const fftc_plan* p, char* buf, size_t len) {
     case KIND_DIST:
       n += dist_describe(p->dist, tmp + n, sizeof(tmp) - n);
       break;
+    case KIND_GPASS:
+      n += snprintf(tmp + n, sizeof(tmp) - n, "kind=gpass N=%lld batch=%lld sign=%d passes=", (long long)p->N,
+                    (long long)p->batch, p->sign);
+      for (int s = 0; s < p->gp.p; ++s) {
+        n += snprintf(tmp + n, sizeof(tmp) - n, "%s%d(", s ? "," : "", p->gp.st[s].L);
+        rad(p->gp.st[s].R, p->gp.st[s].S);
+        n += snprintf(tmp + n, sizeof(tmp) - n, ")");
+      }
+      n += snprintf(tmp + n, sizeof(tmp) - n, " workspace=%lld launches=%d",
+                    (long long)(p->gp.p > 1 ? p->N * p->batch * (int64_t)sizeof(float2) : 0), p->gp.p);
+      break;
     case KIND_L2:
       n += snprintf(tmp + n, sizeof(tmp) - n, "kind=l2 N=%lld batch=%lld sign=%d passes=", (long long)p->N,
                     (long long)p->batch, p->sign);
@@ -435,5 +487,7 @@ int fftc_factorize(int64_t N, int* radices, int max) { return single_pass_radice
 int fftc_plan_split(int64_t N, int64_t* M, int64_t* K) { return top_split(N, M, K); }
 
 int fftc_plan_passes(int64_t N, int* lengths, int max) { return pass_split(N, lengths, max); }
+
+int fftc_plan_gpasses(int64_t N, int* lengths, int max) { return gpass_split(N, lengths, max); }
 
 }  // extern "C"

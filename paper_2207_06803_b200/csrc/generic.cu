@@ -5,7 +5,7 @@
 // stage as fused.cuh (one level of Eq. 2 per stage), but the
 // stage list is a kernel argument, loops are runtime, and stages ping-pong
 // between two shared-memory buffers.
-#include "fused.cuh"
+#include "genstage.cuh"
 #include "registry.h"
 
 namespace fftc {
@@ -13,25 +13,6 @@ namespace fftc {
 namespace {
 
 constexpr int kGenThreads = 256;
-
-template <int R>
-__device__ __forceinline__ void gen_butterfly(const float2* __restrict__ a, float2* __restrict__ b, int N,
-                                              int Ns, int j, const float2* __restrict__ tw) {
-  const int NB = N / R;
-  float2 v[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) v[r] = a[j + r * NB];
-  const int m = j % Ns;
-  if (Ns > 1) {
-    const float2* t = tw + (Ns - 1) + m;
-#pragma unroll
-    for (int r = 1; r < R; ++r) v[r] = cmul(v[r], __ldg(t + (r - 1) * Ns));
-  }
-  Codelet<R>::run(v);
-  const int o = (j / Ns) * Ns * R + m;
-#pragma unroll
-  for (int r = 0; r < R; ++r) b[o + r * Ns] = v[r];
-}
 
 __global__ void __launch_bounds__(kGenThreads)
     k_generic(const float2* __restrict__ in, float2* __restrict__ out, const float2* __restrict__ tw,
@@ -59,18 +40,7 @@ __global__ void __launch_bounds__(kGenThreads)
       const int f = q / NB, j = q % NB;
       const float2* a = A + (size_t)f * N;
       float2* b = B + (size_t)f * N;
-      switch (R) {
-        case 2: gen_butterfly<2>(a, b, N, Ns, j, tw); break;
-        case 3: gen_butterfly<3>(a, b, N, Ns, j, tw); break;
-        case 4: gen_butterfly<4>(a, b, N, Ns, j, tw); break;
-        case 5: gen_butterfly<5>(a, b, N, Ns, j, tw); break;
-        case 7: gen_butterfly<7>(a, b, N, Ns, j, tw); break;
-        case 8: gen_butterfly<8>(a, b, N, Ns, j, tw); break;
-        case 9: gen_butterfly<9>(a, b, N, Ns, j, tw); break;
-        case 16: gen_butterfly<16>(a, b, N, Ns, j, tw); break;
-        case 25: gen_butterfly<25>(a, b, N, Ns, j, tw); break;
-        default: break;
-      }
+      gen_butterfly_rt(R, a, b, N, Ns, j, tw);
     }
     __syncthreads();
     float2* t = A;

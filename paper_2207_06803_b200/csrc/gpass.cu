@@ -1,0 +1,159 @@
+// gpass.cu -- runtime-schedule multi-pass path for any 7-smooth N > 4096 (product path).
+//
+// The compiled large-N kernels (passes.cu) cover powers of two.  Every other 7-smooth N
+// above the single-pass limit runs here: N = L_0 L_1 ... L_{p-1} (each L_s <= 256, a
+// product of generic codelet radices), one HBM pass per factor, each pass one level of
+// the paper's Eq. 2 in Stockham form (SURVEY App. A.2 with radix -> L_s):
+//   column c < N/L, Ns = L_0 ... L_{s-1}:
+//     v[r]  = a[c + r N/L] * w_{Ns L}^{(c mod Ns) r}           (Pi folded into the read; D)
+//     v     = DFT_L v          (runtime Stockham sub-stages over the generic radices)
+//     b[(c div Ns) Ns L + (c mod Ns) + r Ns] = v[r]
+// A CTA owns 16 adjacent columns (ragged at the right edge): coalesced loads with lanes
+// walking columns, the DFT_L's in shared memory (one padded row per column, ping-pong
+// buffers), and stores with lanes walking columns (Ns > 1: 16 columns are adjacent in the
+// output) or walking r (Ns = 1: a column's outputs are contiguous).  Plain loads/stores,
+// not TMA: for odd N the row pitch N/L * 8 bytes is not a multiple of 16.
+#include <vector>
+
+#include "colfft.cuh"
+#include "genstage.cuh"
+#include "gpass.h"
+
+namespace fftc {
+
+namespace {
+
+constexpr int kGpThreads = 256;
+constexpr int kGpCols = 16;
+
+__global__ void __launch_bounds__(kGpThreads)
+    k_gpass(const float2* __restrict__ in, float2* __restrict__ out, GPassStage g, long long N, int tiles,
+            float csign_in, float csign_out) {
+  extern __shared__ float2 sm[];
+  const int L = g.L, LP = L + 1;  // odd column pitch: lanes walking columns hit distinct banks
+  const long long NB = N / L;
+  const long long b = blockIdx.x / tiles;
+  const long long c0 = (long long)(blockIdx.x % tiles) * kGpCols;
+  const int nc = (int)(NB - c0 < kGpCols ? NB - c0 : kGpCols);
+  float2* A = sm;
+  float2* B = sm + kGpCols * LP;
+  const float2* gi = in + b * N + c0;
+  // stage in: lanes walk columns, rows r = e / 16; input twiddle w_T^{(c mod Ns) r}, T = Ns L
+  for (int e = threadIdx.x; e < kGpCols * L; e += kGpThreads) {
+    const int f = e % kGpCols, r = e / kGpCols;
+    if (f < nc) {
+      float2 v = __ldcs(gi + f + (long long)r * NB);
+      v.y *= csign_in;
+      if (g.Ns > 1) v = cmul(v, root_lookup(g.twA, g.twB, (long long)((c0 + f) % g.Ns) * r));
+      A[f * LP + r] = v;
+    }
+  }
+  __syncthreads();
+  // DFT_L of each column: runtime Stockham sub-stages, ping-pong between A and B
+  int ns = 1;
+  for (int s = 0; s < g.S; ++s) {
+    const int R = g.R[s];
+    const int NBs = L / R;
+    for (int q = threadIdx.x; q < nc * NBs; q += kGpThreads) {
+      const int f = q / NBs, j = q % NBs;
+      gen_butterfly_rt(R, A + f * LP, B + f * LP, L, ns, j, g.tw);
+    }
+    __syncthreads();
+    float2* t = A;
+    A = B;
+    B = t;
+    ns *= R;
+  }
+  // stage out
+  float2* go = out + b * N;
+  if (g.Ns == 1) {
+    // column c's outputs are contiguous at c L + r: lanes walk r
+    for (int e = threadIdx.x; e < nc * L; e += kGpThreads) {
+      const int f = e / L, r = e % L;
+      const float2 v = A[f * LP + r];
+      __stcs(go + (c0 + f) * L + r, make_float2(v.x, csign_out * v.y));
+    }
+  } else {
+    for (int e = threadIdx.x; e < kGpCols * L; e += kGpThreads) {
+      const int f = e % kGpCols, r = e / kGpCols;
+      if (f < nc) {
+        const long long c = c0 + f;
+        const float2 v = A[f * LP + r];
+        __stcs(go + (c / g.Ns) * g.Ns * L + (c % g.Ns) + (long long)r * g.Ns, make_float2(v.x, csign_out * v.y));
+      }
+    }
+  }
+}
+
+}  // namespace
+
+int gpass_split(long long N, int* Ls, int max) {
+  if (N <= 4096) return -1;
+  std::vector<int> f;
+  long long n = N;
+  for (int p : {7, 5, 3, 2})
+    while (n % p == 0) {
+      f.push_back(p);
+      n /= p;
+    }
+  if (n != 1) return -1;
+  // fewest passes: largest-first assignment of the prime factors to the group with the
+  // smallest product, every group <= kGpassMaxL
+  for (int p = 2; p <= max; ++p) {
+    std::vector<long long> g((size_t)p, 1);
+    bool ok = true;
+    for (int x : f) {
+      size_t best = 0;
+      for (size_t i = 1; i < g.size(); ++i)
+        if (g[i] < g[best]) best = i;
+      if (g[best] * x > kGpassMaxL) {
+        ok = false;
+        break;
+      }
+      g[best] *= x;
+    }
+    if (!ok) continue;
+    std::vector<long long> s = g;
+    for (size_t i = 0; i < s.size(); ++i)  // descending
+      for (size_t j = i + 1; j < s.size(); ++j)
+        if (s[j] > s[i]) {
+          long long t = s[i];
+          s[i] = s[j];
+          s[j] = t;
+        }
+    for (int i = 0; i < p; ++i) Ls[i] = (int)s[(size_t)i];
+    return p;
+  }
+  return -1;
+}
+
+cudaError_t gpass_execute(const GPassPlanData& d, const float2* in, float2* out, float2* work, long long batch,
+                          int conj, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_gpass, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(2 * kGpCols * (kGpassMaxL + 1) * sizeof(float2)));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const float2* src = in;
+  for (int s = 0; s < d.p; ++s) {
+    float2* dst = ((d.p - 1 - s) % 2 == 0) ? out : work;  // the last pass lands in out
+    const GPassStage& g = d.st[s];
+    const long long NB = d.N / g.L;
+    const int tiles = (int)((NB + kGpCols - 1) / kGpCols);
+    const long long grid = batch * tiles;
+    if (grid > 0x7fffffffLL) return cudaErrorInvalidValue;
+    if (grid > 0) {
+      const size_t smem = (size_t)2 * kGpCols * (g.L + 1) * sizeof(float2);
+      k_gpass<<<(unsigned)grid, kGpThreads, smem, st>>>(src, dst, g, d.N, tiles, (conj && s == 0) ? -1.f : 1.f,
+                                                          (conj && s == d.p - 1) ? -1.f : 1.f);
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+    }
+    src = dst;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace fftc

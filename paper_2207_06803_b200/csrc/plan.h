@@ -4,13 +4,14 @@
 #include <stdint.h>
 
 #include "fourstep.h"
+#include "gpass.h"
 #include "l2pass.h"
 #include "passes.h"
 #include "registry.h"
 
 namespace fftc {
 
-enum PlanKind : int { KIND_COPY = 0, KIND_FUSED = 1, KIND_GENERIC = 2, KIND_FOURSTEP = 3, KIND_DIST = 4, KIND_PASSES = 5, KIND_L2 = 6 };
+enum PlanKind : int { KIND_COPY = 0, KIND_FUSED = 1, KIND_GENERIC = 2, KIND_FOURSTEP = 3, KIND_DIST = 4, KIND_PASSES = 5, KIND_L2 = 6, KIND_GPASS = 7 };
 
 struct DistState;  // dist.cu
 
@@ -46,6 +47,9 @@ struct fftc_plan {
   fftc::PassPlanData pp;
   // L2-resident multi-pass path (power-of-two N in 2^13..2^21)
   fftc::L2PlanData l2;
+  // runtime-schedule multi-pass path (7-smooth N > 4096 that is not a power of two)
+  fftc::GPassPlanData gp;
+  float2* gp_tables[3 * fftc::kMaxGPasses] = {};  // device tables owned by gp (const in GPassStage)
   // host-buffer execution
   fftc::HostStage* hs = nullptr;
   // distributed six-step

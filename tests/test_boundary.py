@@ -98,6 +98,33 @@ def test_planner_passes():
     assert fftc.fftc_plan_passes(256) is None
 
 
+def _smooth(n):
+    for p in (2, 3, 5, 7):
+        while n % p == 0:
+            n //= p
+    return n == 1
+
+
+def test_planner_gpasses():
+    """Runtime-schedule multi-pass split: product N, lengths <= 256 and 7-smooth, fewest
+    passes (a lower bound is ceil(log_256 N)), longest first, deterministic."""
+    sizes = [4097 - 1 + 3 * 2, 12288, 13122, 15625, 16807, 19683, 40960, 46656, 59049, 78125, 100000,
+             248832, 10 ** 6, 3 ** 13, 3 ** 15, 5 ** 10, 7 ** 8, 6 ** 10]
+    for N in sizes:
+        if not _smooth(N):
+            continue
+        Ls = fftc.fftc_plan_gpasses(N)
+        assert Ls is not None, N
+        assert math.prod(Ls) == N and all(2 <= L <= 256 and _smooth(L) for L in Ls), (N, Ls)
+        assert len(Ls) >= math.ceil(math.log(N, 256) - 1e-12) and 2 <= len(Ls) <= 4
+        assert Ls == sorted(Ls, reverse=True)
+        assert Ls == fftc.fftc_plan_gpasses(N)
+    assert fftc.fftc_plan_gpasses(3 ** 10) == [243, 243]
+    assert fftc.fftc_plan_gpasses(4096) is None        # single pass
+    assert fftc.fftc_plan_gpasses(11 * 4096) is None   # prime factor > 7
+    assert fftc.fftc_plan_gpasses(257 * 257) is None   # prime 257
+
+
 def test_no_device_fails_loudly():
     import torch
     if torch.cuda.is_available():

@@ -112,6 +112,44 @@ def test_every_pass_candidate(n, name, monkeypatch):
         check(gpu_fft(x, sign), x, sign)
 
 
+# ---------------------------------------------------------------- any 7-smooth N > 4096
+GPASS = [(12288, 9), (13122, 7), (15625, 5), (16807, 5), (19683, 5), (40960, 3), (46656, 3), (59049, 3),
+         (78125, 2), (100000, 2), (248832, 2), (10 ** 6, 1), (3 ** 13, 1)]
+
+
+@pytest.mark.parametrize("N,batch", GPASS)
+def test_gpass_non_pow2_large(N, batch):
+    """Non-power-of-two N above the single-pass limit: runtime-schedule passes (gpass.cu),
+    odd row pitches, ragged column tiles, both signs, against the oracle."""
+    x = synth.uniform_c64(N, batch, seed=N % 1000)
+    with fftc.Plan(N, batch, -1) as p:
+        assert "kind=gpass" in p.describe(), p.describe()
+        assert p.launches() == len(fftc.fftc_plan_gpasses(N))
+    for sign in (-1, 1):
+        check(gpu_fft(x, sign), x, sign)
+
+
+@pytest.mark.parametrize("n", [13, 16, 20])
+def test_gpass_forced_pow2(n, monkeypatch):
+    """The runtime-schedule passes on powers of two (FFTC_LARGE=gpass) against the oracle."""
+    monkeypatch.setenv("FFTC_LARGE", "gpass")
+    N = 1 << n
+    x = synth.uniform_c64(N, 3, seed=n)
+    with fftc.Plan(N, 3, 1) as p:
+        assert "kind=gpass" in p.describe()
+    check(gpu_fft(x, 1), x, 1)
+
+
+def test_gpass_config4_sized():
+    """A C4-sized non-power-of-two transform: 3^15 (two 243-passes would not fit: three passes)."""
+    N = 3 ** 15
+    x = synth.normal_c64(N, 1, seed=15)
+    with fftc.Plan(N, 1, -1) as p:
+        assert "kind=gpass" in p.describe()
+    y = gpu_fft(x, -1)
+    check(y, x, -1)
+
+
 # ---------------------------------------------------------------- L2-resident multi-pass path
 L2_CASES = [(13, 83), (14, 37), (15, 21), (16, 11), (17, 7), (18, 5), (19, 4), (20, 3), (21, 2)]
 
