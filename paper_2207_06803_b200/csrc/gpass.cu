@@ -8,8 +8,8 @@
 //     v[r]  = a[c + r N/L] * w_{Ns L}^{(c mod Ns) r}           (Pi folded into the read; D)
 //     v     = DFT_L v          (runtime Stockham sub-stages over the generic radices)
 //     b[(c div Ns) Ns L + (c mod Ns) + r Ns] = v[r]
-// A CTA owns 16 adjacent columns (ragged at the right edge): coalesced loads with lanes
-// walking columns, the DFT_L's in shared memory (one padded row per column, ping-pong
+// A CTA owns clamp(4096 / L, 16, 256) adjacent columns (ragged at the right edge):
+// coalesced loads with lanes walking columns, the DFT_L's in shared memory (one padded row per column, ping-pong
 // buffers), and stores with lanes walking columns (Ns > 1: 16 columns are adjacent in the
 // output) or walking r (Ns = 1: a column's outputs are contiguous).  Plain loads/stores,
 // not TMA: for odd N the row pitch N/L * 8 bytes is not a multiple of 16.
@@ -24,27 +24,43 @@ namespace fftc {
 namespace {
 
 constexpr int kGpThreads = 256;
-constexpr int kGpCols = 16;
+constexpr int kGpTile = 4096;  // elements per CTA tile: cols = clamp(4096 / L, 16, 256) columns (power of two)
 
-__global__ void __launch_bounds__(kGpThreads)
+__host__ __device__ inline int gpass_cols(int L) {
+  int c = 16;
+  while (c < 256 && 2 * c * L <= kGpTile) c *= 2;
+  return c;
+}
+
+__global__ void __launch_bounds__(kGpThreads, 4)
     k_gpass(const float2* __restrict__ in, float2* __restrict__ out, GPassStage g, long long N, int tiles,
             float csign_in, float csign_out) {
   extern __shared__ float2 sm[];
+  __shared__ int s_cq[256], s_cm[256], s_R[kMaxStages];
   const int L = g.L, LP = L + 1;  // odd column pitch: lanes walking columns hit distinct banks
+  const int cols = gpass_cols(L), lc = __ffs(cols) - 1;
   const long long NB = N / L;
   const long long b = blockIdx.x / tiles;
-  const long long c0 = (long long)(blockIdx.x % tiles) * kGpCols;
-  const int nc = (int)(NB - c0 < kGpCols ? NB - c0 : kGpCols);
+  const long long c0 = (long long)(blockIdx.x % tiles) * cols;
+  const int nc = (int)(NB - c0 < cols ? NB - c0 : cols);
   float2* A = sm;
-  float2* B = sm + kGpCols * LP;
+  float2* B = sm + cols * LP;
+  // per-column index arithmetic once, in 32 bits (c < N / L < 2^31)
+  if (threadIdx.x < kMaxStages) s_R[threadIdx.x] = threadIdx.x < g.S ? g.R[threadIdx.x] : 1;
+  for (int f = threadIdx.x; f < cols; f += kGpThreads) {
+    const int c = (int)c0 + f;
+    s_cq[f] = c / g.Ns;
+    s_cm[f] = c - (c / g.Ns) * g.Ns;
+  }
+  __syncthreads();
+  // stage in: lanes walk columns; input twiddle w_T^{(c mod Ns) r}, T = Ns L
   const float2* gi = in + b * N + c0;
-  // stage in: lanes walk columns, rows r = e / 16; input twiddle w_T^{(c mod Ns) r}, T = Ns L
-  for (int e = threadIdx.x; e < kGpCols * L; e += kGpThreads) {
-    const int f = e % kGpCols, r = e / kGpCols;
+  for (int e = threadIdx.x; e < (L << lc); e += kGpThreads) {
+    const int f = e & (cols - 1), r = e >> lc;
     if (f < nc) {
       float2 v = __ldcs(gi + f + (long long)r * NB);
       v.y *= csign_in;
-      if (g.Ns > 1) v = cmul(v, root_lookup(g.twA, g.twB, (long long)((c0 + f) % g.Ns) * r));
+      if (g.Ns > 1) v = cmul(v, root_lookup(g.twA, g.twB, (long long)s_cm[f] * r));
       A[f * LP + r] = v;
     }
   }
@@ -52,10 +68,10 @@ __global__ void __launch_bounds__(kGpThreads)
   // DFT_L of each column: runtime Stockham sub-stages, ping-pong between A and B
   int ns = 1;
   for (int s = 0; s < g.S; ++s) {
-    const int R = g.R[s];
+    const int R = s_R[s];
     const int NBs = L / R;
     for (int q = threadIdx.x; q < nc * NBs; q += kGpThreads) {
-      const int f = q / NBs, j = q % NBs;
+      const int f = q / NBs, j = q - (q / NBs) * NBs;
       gen_butterfly_rt(R, A + f * LP, B + f * LP, L, ns, j, g.tw);
     }
     __syncthreads();
@@ -69,17 +85,17 @@ __global__ void __launch_bounds__(kGpThreads)
   if (g.Ns == 1) {
     // column c's outputs are contiguous at c L + r: lanes walk r
     for (int e = threadIdx.x; e < nc * L; e += kGpThreads) {
-      const int f = e / L, r = e % L;
+      const int f = e / L, r = e - (e / L) * L;
       const float2 v = A[f * LP + r];
       __stcs(go + (c0 + f) * L + r, make_float2(v.x, csign_out * v.y));
     }
   } else {
-    for (int e = threadIdx.x; e < kGpCols * L; e += kGpThreads) {
-      const int f = e % kGpCols, r = e / kGpCols;
+    // lanes walk columns: adjacent columns are adjacent in the output (within an Ns block)
+    for (int e = threadIdx.x; e < (L << lc); e += kGpThreads) {
+      const int f = e & (cols - 1), r = e >> lc;
       if (f < nc) {
-        const long long c = c0 + f;
         const float2 v = A[f * LP + r];
-        __stcs(go + (c / g.Ns) * g.Ns * L + (c % g.Ns) + (long long)r * g.Ns, make_float2(v.x, csign_out * v.y));
+        __stcs(go + ((long long)s_cq[f] * L + r) * g.Ns + s_cm[f], make_float2(v.x, csign_out * v.y));
       }
     }
   }
@@ -132,7 +148,7 @@ cudaError_t gpass_execute(const GPassPlanData& d, const float2* in, float2* out,
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k_gpass, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(2 * kGpCols * (kGpassMaxL + 1) * sizeof(float2)));
+                                         (int)(2 * 256 * 17 * sizeof(float2)));  // max over L of 2 cols (L+1)
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -141,11 +157,12 @@ cudaError_t gpass_execute(const GPassPlanData& d, const float2* in, float2* out,
     float2* dst = ((d.p - 1 - s) % 2 == 0) ? out : work;  // the last pass lands in out
     const GPassStage& g = d.st[s];
     const long long NB = d.N / g.L;
-    const int tiles = (int)((NB + kGpCols - 1) / kGpCols);
+    const int cols = gpass_cols(g.L);
+    const int tiles = (int)((NB + cols - 1) / cols);
     const long long grid = batch * tiles;
     if (grid > 0x7fffffffLL) return cudaErrorInvalidValue;
     if (grid > 0) {
-      const size_t smem = (size_t)2 * kGpCols * (g.L + 1) * sizeof(float2);
+      const size_t smem = (size_t)2 * cols * (g.L + 1) * sizeof(float2);
       k_gpass<<<(unsigned)grid, kGpThreads, smem, st>>>(src, dst, g, d.N, tiles, (conj && s == 0) ? -1.f : 1.f,
                                                           (conj && s == d.p - 1) ? -1.f : 1.f);
       cudaError_t e = cudaGetLastError();
