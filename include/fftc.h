@@ -123,6 +123,39 @@ int fftc_plan_passes(int64_t N, int* lengths, int max);
 int fftc_plan_gpasses(int64_t N, int* lengths, int max);
 
 /* ---------------------------------------------------------------------
+ * FFTc factorization expressions (the paper's DSL front end, P:100-121,
+ * Listing 1 / Table 1): e.g.
+ *   (DFT(2) ⊗ I(2)) · twiddle(4,2) · (I(2) ⊗ DFT(2)) · Permute(4,2)
+ * '⊗' (U+2297) or '&' is the Kronecker product, '·' (U+00B7), '*' or '@'
+ * the matrix product; DFT(n), I(n), twiddle(N,M) = D^N_M, Permute(N,K) =
+ * Pi^N_K.  The expression must be Eq. 2 applied recursively,
+ *   (DFT_K ⊗ I_M) · twiddle(N,M) · (I_K ⊗ X_M) · Permute(N,K),  N = M K,
+ * X_M = DFT(M) or again such a factorization (a factored outer DFT_K is
+ * flattened into consecutive stages); or a bare DFT(N) (planner's choice).
+ * An optional "var name =" prefix, trailing ';' and trailing input
+ * identifier (Listing 1's "· InputComplex") are ignored.
+ * ------------------------------------------------------------------- */
+
+/* Host only: parse `expr`, write N and its radix schedule R_0..R_{S-1}
+ * (R_0 = innermost DFT, the executed Stockham stage order).  Returns S
+ * (0 for a bare DFT(N)), or -1 with a message in err (NUL-terminated,
+ * truncated to errlen; err may be NULL).                                  */
+int fftc_expr_radices(const char* expr, int64_t* N, int* radices, int max, char* err, size_t errlen);
+
+/* Plan with an explicit radix schedule (product = N, each >= 2; S = 0:
+ * planner's choice).  N <= 4096: a compiled schedule with exactly these
+ * stages if there is one, else the runtime-schedule kernel (radices from
+ * {16, 8, 4, 2, 9, 3, 25, 5, 7}); N > 4096: consecutive stages grouped
+ * into at most 4 passes of length <= 256.  NULL on failure: INVALID_VALUE
+ * (bad product / arguments), UNSUPPORTED_SIZE (a radix outside the
+ * runtime set with no compiled schedule, or too many passes).           */
+fftc_plan* fftc_plan_create_radices(int64_t N, int64_t batch, int sign, const int* radices, int S);
+
+/* fftc_expr_radices + fftc_plan_create_radices.  INVALID_VALUE if the
+ * expression does not parse or is not an Eq. 2 factorization.            */
+fftc_plan* fftc_plan_create_expr(const char* expr, int64_t batch, int sign);
+
+/* ---------------------------------------------------------------------
  * Distributed six-step (one process per GPU, NCCL over NVLink/NVSwitch).
  * A single transform of length N is block-distributed: rank p holds
  * elements [p*N/P, (p+1)*N/P) of the input and of the output, both in

@@ -66,6 +66,10 @@ def load(path: str = LIB_PATH):
         "fftc_candidates": ([i64, ctypes.POINTER(ctypes.c_char_p), i32], i32),
         "fftc_plan_passes": ([i64, ctypes.POINTER(ctypes.c_int), i32], i32),
         "fftc_plan_gpasses": ([i64, ctypes.POINTER(ctypes.c_int), i32], i32),
+        "fftc_expr_radices": ([ctypes.c_char_p, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int), i32,
+                               ctypes.c_char_p, sz], i32),
+        "fftc_plan_create_radices": ([i64, i64, i32, ctypes.POINTER(ctypes.c_int), i32], vp),
+        "fftc_plan_create_expr": ([ctypes.c_char_p, i64, i32], vp),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -134,6 +138,27 @@ def fftc_plan_gpasses(N: int):
     return None if p < 0 else [arr[i] for i in range(p)]
 
 
+def fftc_expr_radices(expr: str):
+    """Parse an FFTc factorization expression -> (N, radices); raises ValueError with the
+    parser's message if it is not Eq. 2 applied recursively."""
+    N = ctypes.c_int64()
+    arr = (ctypes.c_int * 64)()
+    err = ctypes.create_string_buffer(256)
+    S = load().fftc_expr_radices(expr.encode(), ctypes.byref(N), arr, 64, err, 256)
+    if S < 0:
+        raise ValueError(err.value.decode())
+    return N.value, [arr[i] for i in range(S)]
+
+
+def fftc_plan_create_radices(N: int, batch: int, sign: int, radices) -> int:
+    arr = (ctypes.c_int * max(1, len(radices)))(*radices)
+    return load().fftc_plan_create_radices(N, batch, sign, arr, len(radices)) or 0
+
+
+def fftc_plan_create_expr(expr: str, batch: int, sign: int) -> int:
+    return load().fftc_plan_create_expr(expr.encode(), batch, sign) or 0
+
+
 def fftc_plan_split(N: int):
     M, K = ctypes.c_int64(), ctypes.c_int64()
     r = load().fftc_plan_split(N, ctypes.byref(M), ctypes.byref(K))
@@ -170,6 +195,22 @@ class Plan:
         self.handle = _handle if _handle is not None else fftc_plan_create(N, batch, sign)
         if not self.handle:
             raise FFTCError(fftc_last_error(), "fftc_plan_create(N=%d, batch=%d, sign=%d)" % (N, batch, sign))
+
+    @classmethod
+    def from_expr(cls, expr: str, batch: int, sign: int = -1):
+        """Plan from an FFTc factorization expression (Listing 1 syntax)."""
+        N, _ = fftc_expr_radices(expr)
+        h = fftc_plan_create_expr(expr, batch, sign)
+        if not h:
+            raise FFTCError(fftc_last_error(), "fftc_plan_create_expr(%r)" % expr)
+        return cls(N, batch, sign, _handle=h)
+
+    @classmethod
+    def from_radices(cls, N: int, batch: int, sign: int, radices):
+        h = fftc_plan_create_radices(N, batch, sign, list(radices))
+        if not h:
+            raise FFTCError(fftc_last_error(), "fftc_plan_create_radices(N=%d, %s)" % (N, list(radices)))
+        return cls(N, batch, sign, _handle=h)
 
     @classmethod
     def dist(cls, N: int, sign: int, nccl_id: bytes | None, rank: int, nranks: int, loopback: bool = False):

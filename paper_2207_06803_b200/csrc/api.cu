@@ -14,6 +14,7 @@
 
 #include "../../include/fftc.h"
 #include "dist.h"
+#include "expr.h"
 #include "plan.h"
 #include "planner.h"
 
@@ -133,6 +134,49 @@ static void free_plan(fftc_plan* p) {
     delete p->hs;
   }
   delete p;
+}
+
+static void free_plan(fftc_plan* p);
+
+// Runtime-schedule passes (gpass.cu) with explicit lengths and per-pass radices.
+static fftc_status setup_gpass(fftc_plan* p, const int* Lg, int pg, const int (*R)[kMaxStages], const int* S) {
+  cudaError_t err = cudaSuccess;
+  p->kind = KIND_GPASS;
+  p->gp.N = p->N;
+  p->gp.p = pg;
+  int64_t Ns = 1;
+  for (int s = 0; s < pg && err == cudaSuccess; ++s) {
+    GPassStage& g = p->gp.st[s];
+    g.L = Lg[s];
+    g.Ns = (int)Ns;
+    g.S = S[s];
+    if (g.L > kGpassMaxL || g.S < 1 || g.S > kMaxStages) return FFTC_ERROR_UNSUPPORTED_SIZE;
+    int64_t prod = 1;
+    for (int t = 0; t < g.S; ++t) {
+      if (!generic_supports_radix(R[s][t])) return FFTC_ERROR_UNSUPPORTED_SIZE;
+      g.R[t] = R[s][t];
+      prod *= R[s][t];
+    }
+    if (prod != g.L) return FFTC_ERROR_INVALID_VALUE;
+    const int64_t T = Ns * Lg[s];
+    float2* t0 = upload_stage_table(Lg[s], g.R, g.S, &err);
+    p->gp_tables[3 * s] = t0;
+    g.tw = t0;
+    if (err == cudaSuccess) {
+      float2* t1 = upload_root_table(T, T < 4096 ? T : 4096, 1, &err);
+      p->gp_tables[3 * s + 1] = t1;
+      g.twA = t1;
+    }
+    if (err == cudaSuccess) {
+      float2* t2 = upload_root_table(T, (T + 4095) / 4096, 4096, &err);
+      p->gp_tables[3 * s + 2] = t2;
+      g.twB = t2;
+    }
+    Ns = T;
+  }
+  if (err == cudaSuccess && p->batch > 0 && pg > 1)
+    err = cudaMalloc(&p->d_work, (size_t)(p->N * p->batch) * sizeof(float2));
+  return from_cuda(err);
 }
 
 static fftc_plan* fail(fftc_plan* p, fftc_status s) {
@@ -262,35 +306,10 @@ fftc_plan* fftc_plan_create(int64_t N, int64_t batch, int sign) {
     int Lg[kMaxGPasses];
     const int pg = gpass_split(N, Lg, kMaxGPasses);
     if (pg < 0) return fail(p, FFTC_ERROR_UNSUPPORTED_SIZE);
-    p->kind = KIND_GPASS;
-    p->gp.N = N;
-    p->gp.p = pg;
-    int64_t Ns = 1;
-    for (int s = 0; s < pg && err == cudaSuccess; ++s) {
-      GPassStage& g = p->gp.st[s];
-      g.L = Lg[s];
-      g.Ns = (int)Ns;
-      g.S = generic_radices(Lg[s], g.R, kMaxStages);
-      if (g.S < 1) return fail(p, FFTC_ERROR_UNSUPPORTED_SIZE);
-      const int64_t T = Ns * Lg[s];
-      float2* t0 = upload_stage_table(Lg[s], g.R, g.S, &err);
-      p->gp_tables[3 * s] = t0;
-      g.tw = t0;
-      if (err == cudaSuccess) {
-        float2* t1 = upload_root_table(T, T < 4096 ? T : 4096, 1, &err);
-        p->gp_tables[3 * s + 1] = t1;
-        g.twA = t1;
-      }
-      if (err == cudaSuccess) {
-        float2* t2 = upload_root_table(T, (T + 4095) / 4096, 4096, &err);
-        p->gp_tables[3 * s + 2] = t2;
-        g.twB = t2;
-      }
-      Ns = T;
-    }
-    if (err == cudaSuccess && batch > 0 && pg > 1) err = cudaMalloc(&p->d_work, (size_t)(N * batch) * sizeof(float2));
-    if (err != cudaSuccess) return fail(p, from_cuda(err));
-    return p;
+    int R[kMaxGPasses][kMaxStages], S[kMaxGPasses];
+    for (int s = 0; s < pg; ++s) S[s] = generic_radices(Lg[s], R[s], kMaxStages);
+    const fftc_status st = setup_gpass(p, Lg, pg, R, S);
+    return st == FFTC_SUCCESS ? p : fail(p, st);
   }
   // four-step
   if (split < 0) return fail(p, FFTC_ERROR_UNSUPPORTED_SIZE);
@@ -489,5 +508,97 @@ int fftc_plan_split(int64_t N, int64_t* M, int64_t* K) { return top_split(N, M, 
 int fftc_plan_passes(int64_t N, int* lengths, int max) { return pass_split(N, lengths, max); }
 
 int fftc_plan_gpasses(int64_t N, int* lengths, int max) { return gpass_split(N, lengths, max); }
+
+int fftc_expr_radices(const char* expr, int64_t* N, int* radices, int max, char* err, size_t errlen) {
+  int64_t r[64];
+  const int S = expr_radices(expr, N, r, 64, err, errlen);
+  if (S < 0) return -1;
+  if (S > max) {
+    if (err && errlen) snprintf(err, errlen, "more than %d stages", max);
+    return -1;
+  }
+  for (int s = 0; s < S; ++s) {
+    if (r[s] > 0x7fffffff) {
+      if (err && errlen) snprintf(err, errlen, "radix too large");
+      return -1;
+    }
+    if (radices) radices[s] = (int)r[s];
+  }
+  return S;
+}
+
+fftc_plan* fftc_plan_create_radices(int64_t N, int64_t batch, int sign, const int* radices, int S) {
+  g_last = FFTC_SUCCESS;
+  if (N < 1 || batch < 0 || (sign != -1 && sign != 1) || S < 0 || S > kMaxStages || (S > 0 && !radices))
+    return fail(nullptr, FFTC_ERROR_INVALID_VALUE);
+  if (S == 0) return fftc_plan_create(N, batch, sign);
+  int64_t prod = 1;
+  for (int s = 0; s < S; ++s) {
+    if (radices[s] < 2) return fail(nullptr, FFTC_ERROR_INVALID_VALUE);
+    prod *= radices[s];
+    if (prod > N) return fail(nullptr, FFTC_ERROR_INVALID_VALUE);
+  }
+  if (prod != N) return fail(nullptr, FFTC_ERROR_INVALID_VALUE);
+  if (!seven_smooth(N)) return fail(nullptr, FFTC_ERROR_UNSUPPORTED_SIZE);
+  if (batch > 0 && batch > ((int64_t)1 << 60) / (N * 8)) return fail(nullptr, FFTC_ERROR_UNSUPPORTED_SIZE);
+  int dev = 0;
+  fftc_status ds = fftc_check_device(&dev);
+  if (ds != FFTC_SUCCESS) return fail(nullptr, ds);
+  fftc_plan* p = new fftc_plan();
+  p->N = N;
+  p->batch = batch;
+  p->sign = sign;
+  p->device = dev;
+  cudaError_t err = cudaSuccess;
+  if (N <= kGenericMaxN) {
+    // a compiled schedule with exactly these stages, else the runtime-schedule kernel
+    for (int i = 0; i < fused_count(); ++i) {
+      const FusedEntry* e = fused_at(i);
+      if (e->N != N || e->S != S) continue;
+      bool same = true;
+      for (int s = 0; s < S; ++s) same = same && e->R[s] == radices[s];
+      if (!same) continue;
+      p->kind = KIND_FUSED;
+      p->fe = e;
+      p->d_tw = upload_stage_table(N, e->R, e->S, &err);
+      return err == cudaSuccess ? p : fail(p, from_cuda(err));
+    }
+    for (int s = 0; s < S; ++s)
+      if (!generic_supports_radix(radices[s])) return fail(p, FFTC_ERROR_UNSUPPORTED_SIZE);
+    p->kind = KIND_GENERIC;
+    p->gs.N = (int)N;
+    p->gs.S = S;
+    for (int s = 0; s < S; ++s) p->gs.R[s] = radices[s];
+    p->d_tw = upload_stage_table(N, radices, S, &err);
+    return err == cudaSuccess ? p : fail(p, from_cuda(err));
+  }
+  // above the single-pass limit: consecutive stages grouped into passes of <= kGpassMaxL
+  int Lg[kMaxGPasses], R[kMaxGPasses][kMaxStages], Sg[kMaxGPasses];
+  int pg = 0;
+  int64_t cur = 1;
+  for (int s = 0; s < S; ++s) {
+    if (radices[s] > kGpassMaxL) return fail(p, FFTC_ERROR_UNSUPPORTED_SIZE);
+    if (pg == 0 || cur * radices[s] > kGpassMaxL) {
+      if (pg == kMaxGPasses) return fail(p, FFTC_ERROR_UNSUPPORTED_SIZE);
+      Sg[pg] = 0;
+      Lg[pg] = 1;
+      cur = 1;
+      ++pg;
+    }
+    R[pg - 1][Sg[pg - 1]++] = radices[s];
+    Lg[pg - 1] *= radices[s];
+    cur *= radices[s];
+  }
+  const fftc_status st = setup_gpass(p, Lg, pg, R, Sg);
+  return st == FFTC_SUCCESS ? p : fail(p, st);
+}
+
+fftc_plan* fftc_plan_create_expr(const char* expr, int64_t batch, int sign) {
+  int64_t N = 0;
+  int R[kMaxStages];
+  const int S = fftc_expr_radices(expr, &N, R, kMaxStages, nullptr, 0);
+  if (S < 0) return fail(nullptr, FFTC_ERROR_INVALID_VALUE);
+  return fftc_plan_create_radices(N, batch, sign, R, S);
+}
 
 }  // extern "C"
