@@ -41,7 +41,8 @@ typedef enum {
   FFTC_SUCCESS = 0,
   FFTC_ERROR_INVALID_VALUE = 1,    /* N < 1, batch < 0, sign not in {-1,+1}, NULL pointer,
                                       in == out or overlapping buffers */
-  FFTC_ERROR_UNSUPPORTED_SIZE = 2, /* N has a prime factor > 7 (and is > 1); N*batch*8 overflows;
+  FFTC_ERROR_UNSUPPORTED_SIZE = 2, /* N has a prime factor > 7 and is > 4096, or a prime factor > 61,
+                                      or NVRTC is unavailable for a JIT size; N*batch*8 overflows;
                                       dist: nranks does not divide M and K */
   FFTC_ERROR_MISALIGNED = 3,       /* in / out not 16-byte aligned */
   FFTC_ERROR_OUT_OF_MEMORY = 4,    /* twiddle table / workspace allocation failed */
@@ -154,6 +155,24 @@ fftc_plan* fftc_plan_create_radices(int64_t N, int64_t batch, int sign, const in
 /* fftc_expr_radices + fftc_plan_create_radices.  INVALID_VALUE if the
  * expression does not parse or is not an Eq. 2 factorization.            */
 fftc_plan* fftc_plan_create_expr(const char* expr, int64_t batch, int sign);
+
+/* ---------------------------------------------------------------------
+ * JIT mode: an N <= 4096 with prime factors above 7 (up to 61)
+ * gets a single-pass kernel generated for that N -- Stockham stages, each
+ * DFT_R a straight-line codelet emitted by Eq. 2 (primes: conjugate-pair
+ * form of the definition) -- compiled by NVRTC for sm_100a when the plan
+ * is created (fftc_plan_create; cached per N for the process).  Without
+ * libnvrtc such sizes return FFTC_ERROR_UNSUPPORTED_SIZE.
+ * ------------------------------------------------------------------- */
+
+/* Host only: the generated CUDA source for N (NUL-terminated, truncated to
+ * len).  Returns its length, or -1 if N is not a JIT size.                 */
+int fftc_jit_source(int64_t N, char* buf, size_t len);
+
+/* Host only (no device needed): compile the generated source with NVRTC for
+ * sm_100a.  Returns the cubin size (> 0), or < 0 (-1 no NVRTC / not a JIT
+ * size, -4 compile error); the NVRTC log goes to log (may be NULL).        */
+int fftc_jit_compile(int64_t N, char* log, size_t loglen);
 
 /* ---------------------------------------------------------------------
  * Distributed six-step (one process per GPU, NCCL over NVLink/NVSwitch).

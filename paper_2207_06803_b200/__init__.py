@@ -70,6 +70,8 @@ def load(path: str = LIB_PATH):
                                ctypes.c_char_p, sz], i32),
         "fftc_plan_create_radices": ([i64, i64, i32, ctypes.POINTER(ctypes.c_int), i32], vp),
         "fftc_plan_create_expr": ([ctypes.c_char_p, i64, i32], vp),
+        "fftc_jit_source": ([i64, ctypes.c_char_p, sz], i32),
+        "fftc_jit_compile": ([i64, ctypes.c_char_p, sz], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -157,6 +159,22 @@ def fftc_plan_create_radices(N: int, batch: int, sign: int, radices) -> int:
 
 def fftc_plan_create_expr(expr: str, batch: int, sign: int) -> int:
     return load().fftc_plan_create_expr(expr.encode(), batch, sign) or 0
+
+
+def fftc_jit_source(N: int):
+    n = load().fftc_jit_source(N, None, 0)
+    if n < 0:
+        return None
+    buf = ctypes.create_string_buffer(n + 1)
+    load().fftc_jit_source(N, buf, n + 1)
+    return buf.value.decode()
+
+
+def fftc_jit_compile(N: int):
+    """NVRTC-compile the JIT kernel for N (host only) -> (cubin bytes or error code, log)."""
+    log = ctypes.create_string_buffer(1 << 16)
+    r = load().fftc_jit_compile(N, log, 1 << 16)
+    return r, log.value.decode(errors="replace")
 
 
 def fftc_plan_split(N: int):

@@ -80,7 +80,7 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -
     need_link = force or not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs)
     if need_link:
         tmp = LIB + ".tmp%d" % os.getpid()
-        cmd = ["nvcc", "-shared"] + ARCH + ["-o", tmp] + objs + ["-lcudart"]
+        cmd = ["nvcc", "-shared"] + ARCH + ["-o", tmp] + objs + ["-lcudart", "-ldl"]
         if nccl_lib:
             cmd += ["-L" + nccl_lib, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + nccl_lib]
         subprocess.check_call(cmd)

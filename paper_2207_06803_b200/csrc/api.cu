@@ -10,6 +10,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <string>
 #include <vector>
 
 #include "../../include/fftc.h"
@@ -85,6 +86,8 @@ cudaError_t exec_local(const fftc_plan* p, const float2* in, float2* out, long l
       return l2_execute(p->l2, in, out, work, batch, conj, st);
     case KIND_GPASS:
       return gpass_execute(p->gp, in, out, work, batch, conj, st);
+    case KIND_JIT:
+      return jit_launch(p->jk, in, out, p->d_tw, batch, conj, st);
     case KIND_FOURSTEP: {
       const ColGeom g = fourstep_cols_geom(p->ce, p->N, p->K);
       cudaError_t e = p->ce->launch(in, work, p->d_tw, p->d_twA, p->d_twB, g, batch, conj, 0, st);
@@ -202,7 +205,9 @@ extern "C" {
 fftc_plan* fftc_plan_create(int64_t N, int64_t batch, int sign) {
   g_last = FFTC_SUCCESS;
   if (N < 1 || batch < 0 || (sign != -1 && sign != 1)) return fail(nullptr, FFTC_ERROR_INVALID_VALUE);
-  if (!seven_smooth(N)) return fail(nullptr, FFTC_ERROR_UNSUPPORTED_SIZE);
+  int Rj[32];
+  const int Sj = seven_smooth(N) ? -1 : (N <= kGenericMaxN ? jit_radices((int)N, Rj, 32) : -1);
+  if (!seven_smooth(N) && Sj < 0) return fail(nullptr, FFTC_ERROR_UNSUPPORTED_SIZE);
   if (batch > 0 && batch > ((int64_t)1 << 60) / (N * 8)) return fail(nullptr, FFTC_ERROR_UNSUPPORTED_SIZE);
   int dev = 0;
   fftc_status ds = fftc_check_device(&dev);
@@ -213,6 +218,18 @@ fftc_plan* fftc_plan_create(int64_t N, int64_t batch, int sign) {
   p->sign = sign;
   p->device = dev;
   cudaError_t err = cudaSuccess;
+  if (Sj > 0) {
+    // prime factors > 7: a kernel generated for N and compiled now (NVRTC, sm_100a)
+    if (!jit_available()) return fail(p, FFTC_ERROR_UNSUPPORTED_SIZE);
+    p->kind = KIND_JIT;
+    p->jit_S = Sj;
+    for (int s = 0; s < Sj; ++s) p->jit_R[s] = Rj[s];
+    p->jk = jit_get((int)N, &err);
+    if (!p->jk) return fail(p, err == cudaErrorNotSupported ? FFTC_ERROR_UNSUPPORTED_SIZE : from_cuda(err));
+    p->d_tw = upload_stage_table(N, Rj, Sj, &err);
+    if (err != cudaSuccess) return fail(p, from_cuda(err));
+    return p;
+  }
   if (N == 1) {
     p->kind = KIND_COPY;
     return p;
@@ -417,6 +434,7 @@ int fftc_plan_launches(const fftc_plan* p) {
     case KIND_PASSES: return p->batch > 0 ? p->pp.p : 0;
     case KIND_L2: return p->batch > 0 ? 1 : 0;
     case KIND_GPASS: return p->batch > 0 ? p->gp.p : 0;
+    case KIND_JIT: return p->batch > 0 ? 1 : 0;
     case KIND_DIST: return dist_launches(p->dist);
   }
   return -1;
@@ -457,6 +475,13 @@ int fftc_plan_describe(const fftc_plan* p, char* buf, size_t len) {
       break;
     case KIND_DIST:
       n += dist_describe(p->dist, tmp + n, sizeof(tmp) - n);
+      break;
+    case KIND_JIT:
+      n += snprintf(tmp + n, sizeof(tmp) - n, "kind=jit N=%lld batch=%lld sign=%d radices=", (long long)p->N,
+                    (long long)p->batch, p->sign);
+      rad(p->jit_R, p->jit_S);
+      n += snprintf(tmp + n, sizeof(tmp) - n, " kernel=fftc_jit(nvrtc sm_100a) fpb=%d smem=%zu launches=1", p->jk->fpb,
+                    p->jk->smem);
       break;
     case KIND_GPASS:
       n += snprintf(tmp + n, sizeof(tmp) - n, "kind=gpass N=%lld batch=%lld sign=%d passes=", (long long)p->N,
@@ -591,6 +616,28 @@ fftc_plan* fftc_plan_create_radices(int64_t N, int64_t batch, int sign, const in
   }
   const fftc_status st = setup_gpass(p, Lg, pg, R, Sg);
   return st == FFTC_SUCCESS ? p : fail(p, st);
+}
+
+int fftc_jit_source(int64_t N, char* buf, size_t len) {
+  if (N < 2 || N > kGenericMaxN) return -1;
+  const std::string src = jit_source((int)N);
+  if (src.empty()) return -1;
+  if (buf && len) {
+    strncpy(buf, src.c_str(), len - 1);
+    buf[len - 1] = 0;
+  }
+  return (int)src.size();
+}
+
+int fftc_jit_compile(int64_t N, char* log, size_t loglen) {
+  if (N < 2 || N > kGenericMaxN) return -1;
+  std::string cubin, lg;
+  const int rc = jit_compile_cubin((int)N, &cubin, &lg);
+  if (log && loglen) {
+    strncpy(log, lg.c_str(), loglen - 1);
+    log[loglen - 1] = 0;
+  }
+  return rc == 0 ? (int)cubin.size() : rc;
 }
 
 fftc_plan* fftc_plan_create_expr(const char* expr, int64_t batch, int sign) {

@@ -1,0 +1,422 @@
+// jit.cpp -- JIT-compiled codelets for N with prime factors > 7 (product path, host side).
+//
+// The paper distinguishes a JIT mode, in which the transform size is a runtime value and
+// the code is generated and compiled when it is requested, from an AOT mode with the size
+// fixed at compile time, and names FFTW-style generated codelets as the
+// way to go beyond its dense matrices.  The AOT side here is the set of
+// compiled schedules (kernels_*.cu, passes.cu); this file is the JIT side: for an N <= 4096
+// whose prime factors go beyond the compiled codelet set {2, 3, 5, 7} (primes up to
+// kJitMaxPrime), it generates a single-pass Stockham kernel specialised to N -- every
+// stage one level of Eq. 2, every DFT_R a straight-line codelet emitted by the
+// same recursion (R = K M: K M-point codelets on the stride-K sub-vectors, constant
+// twiddles w_R^{rj}, M K-point codelets; a prime R in the conjugate-pair symmetric form
+// of the definition) -- compiles it with NVRTC for sm_100a and loads it through
+// the driver API.  Kernels are cached per N for the life of the process.
+//
+// No link-time dependency: libnvrtc is dlopen'ed on first use and the driver entry points
+// come from cudaGetDriverEntryPoint, so the library still loads where neither exists.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "jit.h"
+
+namespace fftc {
+
+namespace {
+
+// ---------------------------------------------------------------- source generation
+struct Emitter {
+  std::string src;
+  int tmp = 0;
+  std::string fresh() { return "t" + std::to_string(tmp++); }
+  void line(const std::string& l) { src += "  " + l + "\n"; }
+};
+
+std::string flit(double v) {
+  char b[48];
+  snprintf(b, sizeof b, "%.9ef", v);
+  return b;
+}
+
+int smallest_prime(int n) {
+  for (int p = 2; p * p <= n; ++p)
+    if (n % p == 0) return p;
+  return n;
+}
+
+// name = a * w_R^e, w_R = exp(-2 pi i / R); trivial angles resolved
+std::string emit_twiddle(Emitter& E, const std::string& a, long long e, int R) {
+  e %= R;
+  if (e < 0) e += R;
+  if (e == 0) return a;
+  const std::string t = E.fresh();
+  if ((8 * e) % R == 0) {
+    const int k8 = (int)((8 * e) / R);  // angle -k8 pi / 4
+    const std::string h = "0.70710678118654752f";
+    switch (k8) {
+      case 2: E.line("const cf " + t + " = cf{" + a + ".y, -" + a + ".x};"); break;
+      case 4: E.line("const cf " + t + " = cf{-" + a + ".x, -" + a + ".y};"); break;
+      case 6: E.line("const cf " + t + " = cf{-" + a + ".y, " + a + ".x};"); break;
+      case 1: E.line("const cf " + t + " = cf{(" + a + ".x + " + a + ".y) * " + h + ", (" + a + ".y - " + a + ".x) * " + h + "};"); break;
+      case 3: E.line("const cf " + t + " = cf{(" + a + ".y - " + a + ".x) * " + h + ", -(" + a + ".x + " + a + ".y) * " + h + "};"); break;
+      case 5: E.line("const cf " + t + " = cf{-(" + a + ".x + " + a + ".y) * " + h + ", (" + a + ".x - " + a + ".y) * " + h + "};"); break;
+      default: E.line("const cf " + t + " = cf{(" + a + ".x - " + a + ".y) * " + h + ", (" + a + ".x + " + a + ".y) * " + h + "};"); break;
+    }
+    return t;
+  }
+  const double ang = 2.0 * M_PI * (double)e / (double)R;
+  const std::string c = flit(cos(ang)), s = flit(-sin(ang));
+  E.line("const cf " + t + " = cf{fmaf(" + a + ".x, " + c + ", -" + a + ".y * " + s + "), fmaf(" + a + ".x, " + s +
+         ", " + a + ".y * " + c + ")};");
+  return t;
+}
+
+// y = DFT_R x (forward), straight-line; returns the output variable names.
+std::vector<std::string> emit_dft(Emitter& E, const std::vector<std::string>& x) {
+  const int R = (int)x.size();
+  if (R == 1) return x;
+  if (R == 2) {
+    const std::string a = E.fresh(), b = E.fresh();
+    E.line("const cf " + a + " = cf{" + x[0] + ".x + " + x[1] + ".x, " + x[0] + ".y + " + x[1] + ".y};");
+    E.line("const cf " + b + " = cf{" + x[0] + ".x - " + x[1] + ".x, " + x[0] + ".y - " + x[1] + ".y};");
+    return {a, b};
+  }
+  const int p = smallest_prime(R);
+  if (p == R) {
+    // prime: conjugate-pair symmetric form of y_k = sum_n x_n w^{nk}
+    const int h = (R - 1) / 2;
+    std::vector<std::string> s(h + 1), d(h + 1);
+    for (int j = 1; j <= h; ++j) {
+      s[j] = E.fresh();
+      d[j] = E.fresh();
+      E.line("const cf " + s[j] + " = cf{" + x[j] + ".x + " + x[R - j] + ".x, " + x[j] + ".y + " + x[R - j] + ".y};");
+      E.line("const cf " + d[j] + " = cf{" + x[j] + ".x - " + x[R - j] + ".x, " + x[j] + ".y - " + x[R - j] + ".y};");
+    }
+    std::vector<std::string> y(R);
+    y[0] = E.fresh();
+    {
+      std::string ex = x[0] + ".x", ey = x[0] + ".y";
+      for (int j = 1; j <= h; ++j) {
+        ex += " + " + s[j] + ".x";
+        ey += " + " + s[j] + ".y";
+      }
+      E.line("const cf " + y[0] + " = cf{" + ex + ", " + ey + "};");
+    }
+    for (int k = 1; k <= h; ++k) {
+      const std::string A = E.fresh(), B = E.fresh();
+      std::string ax = x[0] + ".x", ay = x[0] + ".y", bx = "0.f", by = "0.f";
+      for (int j = 1; j <= h; ++j) {
+        const double th = 2.0 * M_PI * (double)((long long)j * k % R) / (double)R;
+        ax = "fmaf(" + s[j] + ".x, " + flit(cos(th)) + ", " + ax + ")";
+        ay = "fmaf(" + s[j] + ".y, " + flit(cos(th)) + ", " + ay + ")";
+        bx = "fmaf(" + d[j] + ".x, " + flit(sin(th)) + ", " + bx + ")";
+        by = "fmaf(" + d[j] + ".y, " + flit(sin(th)) + ", " + by + ")";
+      }
+      E.line("const cf " + A + " = cf{" + ax + ", " + ay + "};");
+      E.line("const cf " + B + " = cf{" + bx + ", " + by + "};");
+      y[k] = E.fresh();
+      y[R - k] = E.fresh();
+      // y_k = A - i B, y_{R-k} = A + i B
+      E.line("const cf " + y[k] + " = cf{" + A + ".x + " + B + ".y, " + A + ".y - " + B + ".x};");
+      E.line("const cf " + y[R - k] + " = cf{" + A + ".x - " + B + ".y, " + A + ".y + " + B + ".x};");
+    }
+    return y;
+  }
+  // composite R = K M, Eq. 2: (DFT_K (x) I_M) D^R_M (I_K (x) DFT_M) Pi^R_K
+  const int K = (R % 4 == 0 && R > 4) ? 4 : p, M = R / K;
+  std::vector<std::vector<std::string>> z((size_t)K);
+  for (int r = 0; r < K; ++r) {
+    std::vector<std::string> sub((size_t)M);
+    for (int q = 0; q < M; ++q) sub[q] = x[(size_t)q * K + r];  // Pi^R_K
+    z[r] = emit_dft(E, sub);                                     // I_K (x) DFT_M
+    for (int j = 0; j < M; ++j) z[r][j] = emit_twiddle(E, z[r][j], (long long)r * j, R);  // D^R_M
+  }
+  std::vector<std::string> y((size_t)R);
+  for (int j = 0; j < M; ++j) {
+    std::vector<std::string> col((size_t)K);
+    for (int r = 0; r < K; ++r) col[r] = z[r][j];
+    const std::vector<std::string> o = emit_dft(E, col);  // DFT_K (x) I_M
+    for (int k1 = 0; k1 < K; ++k1) y[(size_t)j + (size_t)M * k1] = o[k1];
+  }
+  return y;
+}
+
+std::string codelet_fn(int R) {
+  Emitter E;
+  std::vector<std::string> x((size_t)R);
+  for (int r = 0; r < R; ++r) {
+    x[r] = "x" + std::to_string(r);
+    E.line("const cf " + x[r] + " = v[" + std::to_string(r) + "];");
+  }
+  const std::vector<std::string> y = emit_dft(E, x);
+  for (int r = 0; r < R; ++r) E.line("v[" + std::to_string(r) + "] = " + y[r] + ";");
+  return "__device__ __forceinline__ void dft" + std::to_string(R) + "(cf* v) {\n" + E.src + "}\n";
+}
+
+}  // namespace
+
+int jit_radices(int N, int* R, int max) {
+  if (N < 2) return -1;
+  std::vector<int> out;
+  int n = N;
+  int a = 0;
+  while (n % 2 == 0) {
+    n /= 2;
+    ++a;
+  }
+  for (int i = 0; i < a / 4; ++i) out.push_back(16);
+  if (a % 4) out.push_back(1 << (a % 4));
+  while (n % 9 == 0) {
+    out.push_back(9);
+    n /= 9;
+  }
+  if (n % 3 == 0) {
+    out.push_back(3);
+    n /= 3;
+  }
+  while (n % 25 == 0) {
+    out.push_back(25);
+    n /= 25;
+  }
+  if (n % 5 == 0) {
+    out.push_back(5);
+    n /= 5;
+  }
+  while (n % 7 == 0) {
+    out.push_back(7);
+    n /= 7;
+  }
+  for (int p = 11; n > 1; p += 2) {
+    if (p > kJitMaxPrime) return -1;
+    while (n % p == 0) {
+      out.push_back(p);
+      n /= p;
+    }
+  }
+  if ((int)out.size() > max) return -1;
+  for (size_t i = 0; i < out.size(); ++i) R[i] = out[i];
+  return (int)out.size();
+}
+
+int jit_fpb(int N) {
+  int f = kJitTile / N;
+  return f < 1 ? 1 : f;
+}
+
+std::string jit_source(int N) {
+  int R[32];
+  const int S = jit_radices(N, R, 32);
+  if (S < 0) return "";
+  const int FPB = jit_fpb(N), NP = N | 1;
+  std::string s;
+  s += "// generated by libfftc (jit.cpp) for N = " + std::to_string(N) + "\n";
+  s += "struct alignas(8) cf { float x, y; };\n";
+  std::vector<int> done;
+  for (int i = 0; i < S; ++i) {
+    bool seen = false;
+    for (int d : done) seen = seen || d == R[i];
+    if (seen) continue;
+    done.push_back(R[i]);
+    s += codelet_fn(R[i]);
+  }
+  char b[512];
+  snprintf(b, sizeof b,
+           "extern \"C\" __global__ void __launch_bounds__(%d) fftc_jit(const cf* __restrict__ in, cf* __restrict__ out,\n"
+           "    const cf* __restrict__ tw, long long batch, float csign) {\n"
+           "  extern __shared__ cf sm[];\n"
+           "  constexpr int N = %d, FPB = %d, NP = %d, T = %d;\n",
+           kJitThreads, N, FPB, NP, kJitThreads);
+  s += b;
+  s += "  const long long f0 = (long long)blockIdx.x * FPB;\n"
+       "  const int nf = (int)(batch - f0 < FPB ? batch - f0 : FPB);\n"
+       "  cf* A = sm; cf* B = sm + FPB * NP;\n"
+       "  const cf* gi = in + f0 * N; cf* go = out + f0 * N;\n"
+       "  for (int e = threadIdx.x; e < nf * N; e += T) { const cf a = gi[e]; A[(e / N) * NP + e % N] = cf{a.x, csign * a.y}; }\n"
+       "  __syncthreads();\n";
+  int Ns = 1;
+  for (int i = 0; i < S; ++i) {
+    const int Rs = R[i], NB = N / Rs;
+    snprintf(b, sizeof b,
+             "  { // stage %d: radix %d, Ns %d\n"
+             "    for (int q = threadIdx.x; q < nf * %d; q += T) {\n"
+             "      const int f = q / %d, j = q %% %d, m = j %% %d;\n"
+             "      const cf* a = A + f * NP; cf* bb = B + f * NP;\n"
+             "      cf v[%d];\n",
+             i, Rs, Ns, NB, NB, NB, Ns, Rs);
+    s += b;
+    snprintf(b, sizeof b, "      for (int r = 0; r < %d; ++r) v[r] = a[j + r * %d];\n", Rs, NB);
+    s += b;
+    if (Ns > 1) {
+      snprintf(b, sizeof b,
+               "      for (int r = 1; r < %d; ++r) { const cf w = tw[%d + (r - 1) * %d + m];\n"
+               "        v[r] = cf{fmaf(v[r].x, w.x, -v[r].y * w.y), fmaf(v[r].x, w.y, v[r].y * w.x)}; }\n",
+               Rs, Ns - 1, Ns);
+      s += b;
+    }
+    snprintf(b, sizeof b,
+             "      dft%d(v);\n"
+             "      const int o = (j / %d) * %d + m;\n"
+             "      for (int r = 0; r < %d; ++r) bb[o + r * %d] = v[r];\n"
+             "    }\n"
+             "    __syncthreads(); cf* t = A; A = B; B = t;\n"
+             "  }\n",
+             Rs, Ns, Ns * Rs, Rs, Ns);
+    s += b;
+    Ns *= Rs;
+  }
+  s += "  for (int e = threadIdx.x; e < nf * N; e += T) { const cf a = A[(e / N) * NP + e % N]; go[e] = cf{a.x, csign * a.y}; }\n"
+       "}\n";
+  return s;
+}
+
+// ---------------------------------------------------------------- NVRTC + driver API
+namespace {
+
+typedef int (*nvrtcCreateProgram_t)(void**, const char*, const char*, int, const char* const*, const char* const*);
+typedef int (*nvrtcCompileProgram_t)(void*, int, const char* const*);
+typedef int (*nvrtcGetSize_t)(void*, size_t*);
+typedef int (*nvrtcGetData_t)(void*, char*);
+typedef int (*nvrtcDestroyProgram_t)(void**);
+
+struct Nvrtc {
+  bool ok = false;
+  nvrtcCreateProgram_t create = nullptr;
+  nvrtcCompileProgram_t compile = nullptr;
+  nvrtcGetSize_t log_size = nullptr, cubin_size = nullptr;
+  nvrtcGetData_t log = nullptr, cubin = nullptr;
+  nvrtcDestroyProgram_t destroy = nullptr;
+};
+
+const Nvrtc& nvrtc() {
+  static Nvrtc n;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = nullptr;
+    for (const char* name : {"libnvrtc.so.12", "libnvrtc.so", "/usr/local/cuda/lib64/libnvrtc.so.12"}) {
+      h = dlopen(name, RTLD_NOW | RTLD_LOCAL);
+      if (h) break;
+    }
+    if (!h) return;
+    n.create = (nvrtcCreateProgram_t)dlsym(h, "nvrtcCreateProgram");
+    n.compile = (nvrtcCompileProgram_t)dlsym(h, "nvrtcCompileProgram");
+    n.log_size = (nvrtcGetSize_t)dlsym(h, "nvrtcGetProgramLogSize");
+    n.log = (nvrtcGetData_t)dlsym(h, "nvrtcGetProgramLog");
+    n.cubin_size = (nvrtcGetSize_t)dlsym(h, "nvrtcGetCUBINSize");
+    n.cubin = (nvrtcGetData_t)dlsym(h, "nvrtcGetCUBIN");
+    n.destroy = (nvrtcDestroyProgram_t)dlsym(h, "nvrtcDestroyProgram");
+    n.ok = n.create && n.compile && n.log_size && n.log && n.cubin_size && n.cubin && n.destroy;
+  });
+  return n;
+}
+
+template <class F>
+F driver_fn(const char* name) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return (F)p;
+}
+
+std::mutex g_mu;
+std::map<int, JitKernel*> g_cache;
+std::string g_log;
+
+}  // namespace
+
+bool jit_available() { return nvrtc().ok; }
+
+int jit_compile_cubin(int N, std::string* cubin, std::string* log) {
+  const Nvrtc& n = nvrtc();
+  if (!n.ok) return -1;
+  const std::string src = jit_source(N);
+  if (src.empty()) return -2;
+  void* prog = nullptr;
+  if (n.create(&prog, src.c_str(), "fftc_jit.cu", 0, nullptr, nullptr) != 0) return -3;
+  const char* opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-lineinfo"};
+  const int rc = n.compile(prog, 3, opts);
+  size_t ls = 0;
+  n.log_size(prog, &ls);
+  if (log) {
+    log->assign(ls, '\0');
+    if (ls) n.log(prog, &(*log)[0]);
+  }
+  if (rc != 0) {
+    n.destroy(&prog);
+    return -4;
+  }
+  size_t cs = 0;
+  n.cubin_size(prog, &cs);
+  cubin->assign(cs, '\0');
+  n.cubin(prog, &(*cubin)[0]);
+  n.destroy(&prog);
+  return 0;
+}
+
+const JitKernel* jit_get(int N, cudaError_t* err) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = g_cache.find(N);
+  if (it != g_cache.end()) return it->second;
+  typedef CUresult (*load_t)(CUmodule*, const void*);
+  typedef CUresult (*getfn_t)(CUfunction*, CUmodule, const char*);
+  typedef CUresult (*setattr_t)(CUfunction, CUfunction_attribute, int);
+  static load_t load = driver_fn<load_t>("cuModuleLoadData");
+  static getfn_t getfn = driver_fn<getfn_t>("cuModuleGetFunction");
+  static setattr_t setattr = driver_fn<setattr_t>("cuFuncSetAttribute");
+  *err = cudaErrorNotSupported;
+  if (!load || !getfn || !setattr) return nullptr;
+  // the driver-API module load needs the runtime's primary context to be current
+  *err = cudaFree(nullptr);
+  if (*err != cudaSuccess) return nullptr;
+  *err = cudaErrorNotSupported;
+  std::string cubin;
+  if (jit_compile_cubin(N, &cubin, &g_log) != 0) return nullptr;
+  CUmodule mod = nullptr;
+  CUfunction fn = nullptr;
+  if (load(&mod, cubin.data()) != CUDA_SUCCESS || getfn(&fn, mod, "fftc_jit") != CUDA_SUCCESS) {
+    *err = cudaErrorInvalidKernelImage;
+    return nullptr;
+  }
+  JitKernel* k = new JitKernel();
+  k->fn = fn;
+  k->N = N;
+  k->fpb = jit_fpb(N);
+  k->smem = (size_t)2 * k->fpb * (N | 1) * 8;
+  if (setattr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)k->smem) != CUDA_SUCCESS) {
+    delete k;
+    *err = cudaErrorInvalidValue;
+    return nullptr;
+  }
+  g_cache[N] = k;
+  *err = cudaSuccess;
+  return k;
+}
+
+cudaError_t jit_launch(const JitKernel* k, const float2* in, float2* out, const float2* tw, long long batch, int conj,
+                       cudaStream_t st) {
+  typedef CUresult (*launch_t)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
+                               CUstream, void**, void**);
+  static launch_t launch = driver_fn<launch_t>("cuLaunchKernel");
+  if (!launch) return cudaErrorNotSupported;
+  const long long grid = (batch + k->fpb - 1) / k->fpb;
+  if (grid == 0) return cudaSuccess;
+  if (grid > 0x7fffffffLL) return cudaErrorInvalidValue;
+  float csign = conj ? -1.f : 1.f;
+  void* args[] = {(void*)&in, (void*)&out, (void*)&tw, (void*)&batch, (void*)&csign};
+  const CUresult r = launch(k->fn, (unsigned)grid, 1, 1, kJitThreads, 1, 1, (unsigned)k->smem, (CUstream)st, args,
+                            nullptr);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorLaunchFailure;
+}
+
+const char* jit_last_log() { return g_log.c_str(); }
+
+}  // namespace fftc

@@ -1,0 +1,36 @@
+// jit.h -- JIT-compiled kernels for N with prime factors > 7 (product path, host side).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stddef.h>
+
+#include <string>
+
+namespace fftc {
+
+constexpr int kJitMaxPrime = 61;  // largest prime radix the JIT emits (conjugate-pair form, O(p^2))
+constexpr int kJitThreads = 256;
+constexpr int kJitTile = 4096;    // elements per CTA (FPB = 4096 / N transforms)
+
+struct JitKernel {
+  CUfunction fn;
+  int N, fpb;
+  size_t smem;
+};
+
+// Radix schedule for the JIT kernel (16/8/4/2, 9/3, 25/5, 7, then primes 11..kJitMaxPrime),
+// or -1 if N has a prime factor > kJitMaxPrime.
+int jit_radices(int N, int* R, int max);
+int jit_fpb(int N);
+// CUDA C++ source of the kernel specialised to N ("" if unsupported).
+std::string jit_source(int N);
+// NVRTC compile to an sm_100a cubin (no device needed).  0 on success.
+int jit_compile_cubin(int N, std::string* cubin, std::string* log);
+bool jit_available();
+// Compiled + loaded kernel for N (cached per process).
+const JitKernel* jit_get(int N, cudaError_t* err);
+cudaError_t jit_launch(const JitKernel* k, const float2* in, float2* out, const float2* tw, long long batch, int conj,
+                       cudaStream_t st);
+const char* jit_last_log();
+
+}  // namespace fftc

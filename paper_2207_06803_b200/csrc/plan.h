@@ -5,13 +5,14 @@
 
 #include "fourstep.h"
 #include "gpass.h"
+#include "jit.h"
 #include "l2pass.h"
 #include "passes.h"
 #include "registry.h"
 
 namespace fftc {
 
-enum PlanKind : int { KIND_COPY = 0, KIND_FUSED = 1, KIND_GENERIC = 2, KIND_FOURSTEP = 3, KIND_DIST = 4, KIND_PASSES = 5, KIND_L2 = 6, KIND_GPASS = 7 };
+enum PlanKind : int { KIND_COPY = 0, KIND_FUSED = 1, KIND_GENERIC = 2, KIND_FOURSTEP = 3, KIND_DIST = 4, KIND_PASSES = 5, KIND_L2 = 6, KIND_GPASS = 7, KIND_JIT = 8 };
 
 struct DistState;  // dist.cu
 
@@ -50,6 +51,10 @@ struct fftc_plan {
   // runtime-schedule multi-pass path (7-smooth N > 4096 that is not a power of two)
   fftc::GPassPlanData gp;
   float2* gp_tables[3 * fftc::kMaxGPasses] = {};  // device tables owned by gp (const in GPassStage)
+  // JIT-compiled single pass (prime factors > 7): kernel from the per-process cache
+  const fftc::JitKernel* jk = nullptr;
+  int jit_R[32] = {};
+  int jit_S = 0;
   // host-buffer execution
   fftc::HostStage* hs = nullptr;
   // distributed six-step

@@ -310,7 +310,7 @@ def test_boundary_errors():
         assert fftc.fftc_execute(h, x.data_ptr() + 8, y.data_ptr(), 0) == fftc.FFTC_ERROR_MISALIGNED
         assert fftc.fftc_execute(h, x.data_ptr(), y.data_ptr() + 8, 0) == fftc.FFTC_ERROR_MISALIGNED
         assert fftc.fftc_execute(h, x.data_ptr(), y.data_ptr(), 0) == fftc.FFTC_SUCCESS
-    for bad, code in [((0, 1, -1), 1), ((8, 1, 0), 1), ((11, 1, -1), 2), ((8 * 13, 1, -1), 2)]:
+    for bad, code in [((0, 1, -1), 1), ((8, 1, 0), 1), ((67, 1, -1), 2), ((8 * 67, 1, -1), 2)]:
         assert fftc.fftc_plan_create(*bad) == 0
         assert fftc.fftc_last_error() == code
     torch.cuda.synchronize()

@@ -1,0 +1,66 @@
+"""JIT mode: sizes with prime factors above 7.
+
+CPU: the generated source compiles with NVRTC for sm_100a (no device needed), the
+planner rejects what the JIT cannot do.  GPU: parity of the JIT kernels against the
+oracle (whose recursive Cooley-Tukey falls back to the definition for prime lengths).
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+import paper_2207_06803_b200 as fftc
+
+JIT_SIZES = [11, 13, 17, 19, 22, 23, 26, 29, 31, 33, 37, 41, 43, 47, 53, 59, 61, 121, 143, 169, 187, 253, 429,
+             704, 1331, 2 * 61 * 29, 3328, 16 * 11 * 23, 11 * 13 * 17]
+
+
+def _jit(N):
+    return fftc.fftc_jit_source(N) is not None
+
+
+@pytest.mark.parametrize("N", [11, 13, 61, 143, 3328, 2 * 61 * 29])
+def test_jit_source_compiles_for_sm100a(N):
+    r, log = fftc.fftc_jit_compile(N)
+    assert r > 0, log
+
+
+def test_jit_planner_domain():
+    for N in JIT_SIZES:
+        assert _jit(N), N
+    assert not _jit(67)            # prime above 61
+    assert not _jit(64 * 67)
+    assert not _jit(1)
+    assert fftc.fftc_jit_source(4096 * 11) is None  # above the single-pass limit
+
+
+def test_generated_codelet_source_shape():
+    src = fftc.fftc_jit_source(13 * 16)
+    assert "dft13" in src and "dft16" in src and "fftc_jit" in src
+    assert "sm_" not in src  # architecture comes from the NVRTC options, not the source
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N", JIT_SIZES)
+def test_gpu_jit_parity(N):
+    torch = pytest.importorskip("torch")
+    batch = 37
+    x = synth.uniform_c64(N, batch, seed=N)
+    for sign in (-1, 1):
+        with fftc.Plan(N, batch, sign) as p:
+            assert "kind=jit" in p.describe(), p.describe()
+            y = p(torch.from_numpy(x).cuda())
+            torch.cuda.synchronize()
+            y = y.cpu().numpy()
+        err = oracle.rel_l2(y, oracle.fft_ct(x, sign)).max()
+        assert err <= min(oracle.tolerance(N), 2e-6), (N, sign, err)
+
+
+@pytest.mark.gpu
+def test_gpu_jit_unsupported():
+    pytest.importorskip("torch")
+    for N in (67, 64 * 67, 4096 * 11):
+        with pytest.raises(fftc.FFTCError) as e:
+            fftc.Plan(N, 2, -1)
+        assert e.value.status == fftc.FFTC_ERROR_UNSUPPORTED_SIZE
