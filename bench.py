@@ -359,7 +359,8 @@ def run_c5(args):
         nid = bytes(idt.cpu().numpy().tobytes())
     else:
         nid = None
-    plan = fftc.Plan.dist(N, -1, nid, rank, world)
+    lb = args.c5_loopback if world == 1 else 0
+    plan = fftc.Plan.dist(N, -1, nid, rank, lb or world, loopback=bool(lb))
     slab = N // world
     # rank r holds elements [r N/P, (r+1) N/P) of one seeded U[-1,1) vector (generated per slab
     # from a per-rank seed so no rank materialises the whole 8 GiB vector)
@@ -392,7 +393,10 @@ def run_c5(args):
                 "warmup": args.warmup, "ms_per_step": round(t * 1e3 / K, 4), "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f32 (complex64)",
                 "data": "synthetic U[-1,1), per-rank seeded slabs",
-                "config": {"workload": "C5 six-step N=%d over %d rank(s)" % (N, world), "plan": plan.describe(),
+                "config": {"workload": ("C5 six-step N=%d, %d virtual ranks on one GPU (loopback: the three "
+                                        "all-to-alls are device copies)" % (N, lb)) if lb else
+                                       ("C5 six-step N=%d over %d rank(s)" % (N, world)),
+                           "plan": plan.describe(),
                            "nvlink_bytes_per_rank_per_step": a2a_bytes},
                 "gpu_launches": plan.launches() * K, "clocks": sampler.summary()}
         print(json.dumps(line), flush=True)
@@ -435,6 +439,8 @@ def main():
     ap.add_argument("--impl", default="fftc", choices=["fftc", "reference"])
     ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--c5-n", type=int, default=1 << 30)
+    ap.add_argument("--c5-loopback", type=int, default=0,
+                    help="one GPU: run the six-step for P virtual ranks (all-to-alls = device copies)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--graph", action="store_true", help="also time the step captured in a CUDA graph")
     ap.add_argument("--no-cpu", action="store_true")

@@ -174,6 +174,13 @@ int fftc_jit_source(int64_t N, char* buf, size_t len);
  * size, -4 compile error); the NVRTC log goes to log (may be NULL).        */
 int fftc_jit_compile(int64_t N, char* log, size_t loglen);
 
+/* The paper's "direct" DFT: y = DFT_N x as one dense
+ * product per transform, batched into a GEMM on the tcgen05 tensor cores
+ * (kind::tf32, 3xTF32 split for fp32-level accuracy), for N in {16, 32}.
+ * Same layout, signs and errors as fftc_plan_create; UNSUPPORTED_SIZE for
+ * other N.  Opt-in: fftc_plan_create never selects it.                     */
+fftc_plan* fftc_plan_create_direct(int64_t N, int64_t batch, int sign);
+
 /* ---------------------------------------------------------------------
  * Distributed six-step (one process per GPU, NCCL over NVLink/NVSwitch).
  * A single transform of length N is block-distributed: rank p holds

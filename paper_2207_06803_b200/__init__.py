@@ -71,6 +71,7 @@ def load(path: str = LIB_PATH):
         "fftc_plan_create_radices": ([i64, i64, i32, ctypes.POINTER(ctypes.c_int), i32], vp),
         "fftc_plan_create_expr": ([ctypes.c_char_p, i64, i32], vp),
         "fftc_jit_source": ([i64, ctypes.c_char_p, sz], i32),
+        "fftc_plan_create_direct": ([i64, i64, i32], vp),
         "fftc_jit_compile": ([i64, ctypes.c_char_p, sz], i32),
     }
     for name, (args, res) in sig.items():
@@ -221,6 +222,14 @@ class Plan:
         h = fftc_plan_create_expr(expr, batch, sign)
         if not h:
             raise FFTCError(fftc_last_error(), "fftc_plan_create_expr(%r)" % expr)
+        return cls(N, batch, sign, _handle=h)
+
+    @classmethod
+    def direct(cls, N: int, batch: int, sign: int = -1):
+        """The paper's direct DFT as a batched dense product on the tensor cores (N = 16, 32)."""
+        h = load().fftc_plan_create_direct(N, batch, sign) or 0
+        if not h:
+            raise FFTCError(fftc_last_error(), "fftc_plan_create_direct(N=%d)" % N)
         return cls(N, batch, sign, _handle=h)
 
     @classmethod

@@ -88,6 +88,8 @@ cudaError_t exec_local(const fftc_plan* p, const float2* in, float2* out, long l
       return gpass_execute(p->gp, in, out, work, batch, conj, st);
     case KIND_JIT:
       return jit_launch(p->jk, in, out, p->d_tw, batch, conj, st);
+    case KIND_DIRECT:
+      return direct_execute(p->N, in, out, p->d_direct, batch, st);
     case KIND_FOURSTEP: {
       const ColGeom g = fourstep_cols_geom(p->ce, p->N, p->K);
       cudaError_t e = p->ce->launch(in, work, p->d_tw, p->d_twA, p->d_twB, g, batch, conj, 0, st);
@@ -117,6 +119,7 @@ static void free_plan(fftc_plan* p) {
   cudaFree(p->d_twB);
   cudaFree(p->d_work);
   for (int i = 0; i < 3 * kMaxGPasses; ++i) cudaFree(p->gp_tables[i]);
+  cudaFree(p->d_direct);
   for (int s = 0; s < kMaxL2Passes; ++s) {
     cudaFree(p->l2.tw[s]);
     cudaFree(p->l2.twA[s]);
@@ -435,6 +438,7 @@ int fftc_plan_launches(const fftc_plan* p) {
     case KIND_L2: return p->batch > 0 ? 1 : 0;
     case KIND_GPASS: return p->batch > 0 ? p->gp.p : 0;
     case KIND_JIT: return p->batch > 0 ? 1 : 0;
+    case KIND_DIRECT: return p->batch > 0 ? 1 : 0;
     case KIND_DIST: return dist_launches(p->dist);
   }
   return -1;
@@ -475,6 +479,12 @@ int fftc_plan_describe(const fftc_plan* p, char* buf, size_t len) {
       break;
     case KIND_DIST:
       n += dist_describe(p->dist, tmp + n, sizeof(tmp) - n);
+      break;
+    case KIND_DIRECT:
+      n += snprintf(tmp + n, sizeof(tmp) - n,
+                    "kind=direct N=%lld batch=%lld sign=%d kernel=k_direct_tc(tcgen05.mma kind::tf32, 3xTF32, "
+                    "M=128 N=K=%lld) launches=1",
+                    (long long)p->N, (long long)p->batch, p->sign, (long long)(2 * p->N));
       break;
     case KIND_JIT:
       n += snprintf(tmp + n, sizeof(tmp) - n, "kind=jit N=%lld batch=%lld sign=%d radices=", (long long)p->N,
@@ -616,6 +626,26 @@ fftc_plan* fftc_plan_create_radices(int64_t N, int64_t batch, int sign, const in
   }
   const fftc_status st = setup_gpass(p, Lg, pg, R, Sg);
   return st == FFTC_SUCCESS ? p : fail(p, st);
+}
+
+fftc_plan* fftc_plan_create_direct(int64_t N, int64_t batch, int sign) {
+  g_last = FFTC_SUCCESS;
+  if (N < 1 || batch < 0 || (sign != -1 && sign != 1)) return fail(nullptr, FFTC_ERROR_INVALID_VALUE);
+  if (!direct_supported(N)) return fail(nullptr, FFTC_ERROR_UNSUPPORTED_SIZE);
+  if (batch > 0 && batch > ((int64_t)1 << 60) / (N * 8)) return fail(nullptr, FFTC_ERROR_UNSUPPORTED_SIZE);
+  int dev = 0;
+  fftc_status ds = fftc_check_device(&dev);
+  if (ds != FFTC_SUCCESS) return fail(nullptr, ds);
+  fftc_plan* p = new fftc_plan();
+  p->N = N;
+  p->batch = batch;
+  p->sign = sign;
+  p->device = dev;
+  p->kind = KIND_DIRECT;
+  cudaError_t err = cudaSuccess;
+  p->d_direct = direct_tables(N, sign, &err);
+  if (err != cudaSuccess) return fail(p, from_cuda(err));
+  return p;
 }
 
 int fftc_jit_source(int64_t N, char* buf, size_t len) {

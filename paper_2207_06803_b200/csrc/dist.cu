@@ -50,27 +50,24 @@ struct DistState {
 namespace {
 
 // dst[i0*s0 + i1*s1 + i2] = src[(i0*n1 + i1)*n2 + i2] (src contiguous [n0][n1][n2]), optional conj.
-__global__ void k_permute3(const float2* __restrict__ src, float2* __restrict__ dst, long long n0, long long n1,
-                           long long n2, long long s0, long long s1, float csign) {
-  const long long total = n0 * n1 * n2;
-  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
-       t += (long long)gridDim.x * blockDim.x) {
-    const long long i2 = t % n2;
-    const long long r = t / n2;
-    const long long i1 = r % n1, i0 = r / n1;
+// Index decomposition in 32-bit unsigned arithmetic (a rank's slab holds < 2^32 elements).
+__global__ void k_permute3(const float2* __restrict__ src, float2* __restrict__ dst, unsigned n0, unsigned n1,
+                           unsigned n2, long long s0, long long s1, float csign) {
+  const unsigned total = n0 * n1 * n2;
+  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const unsigned r = t / n2, i2 = t - r * n2;
+    const unsigned i0 = r / n1, i1 = r - i0 * n1;
     float2 a = __ldcs(src + t);
     __stcs(dst + i0 * s0 + i1 * s1 + i2, make_float2(a.x, csign * a.y));
   }
 }
 // same with 128-bit element pairs (n2, s0, s1 even; 16-byte aligned buffers)
-__global__ void k_permute3_v2(const float4* __restrict__ src, float2* __restrict__ dst, long long n0, long long n1,
-                              long long n2h, long long s0, long long s1, float csign) {
-  const long long total = n0 * n1 * n2h;
-  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
-       t += (long long)gridDim.x * blockDim.x) {
-    const long long i2 = 2 * (t % n2h);
-    const long long r = t / n2h;
-    const long long i1 = r % n1, i0 = r / n1;
+__global__ void k_permute3_v2(const float4* __restrict__ src, float2* __restrict__ dst, unsigned n0, unsigned n1,
+                              unsigned n2h, long long s0, long long s1, float csign) {
+  const unsigned total = n0 * n1 * n2h;
+  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const unsigned r = t / n2h, i2 = 2 * (t - r * n2h);
+    const unsigned i0 = r / n1, i1 = r - i0 * n1;
     float4 a = __ldcs(src + t);
     __stcs(reinterpret_cast<float4*>(dst + i0 * s0 + i1 * s1 + i2), make_float4(a.x, csign * a.y, a.z, csign * a.w));
   }
@@ -82,17 +79,18 @@ cudaError_t permute3(const float2* src, float2* dst, long long n0, long long n1,
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const float cs = conj ? -1.f : 1.f;
+  if (n0 * n1 * n2 >= (1LL << 32)) return cudaErrorInvalidValue;  // slab beyond 32-bit indexing
   if (n2 % 2 == 0 && s0 % 2 == 0 && s1 % 2 == 0) {
     const long long total = n0 * n1 * (n2 / 2);
     long long blocks = (total + 255) / 256;
     if (blocks > (long long)sms * 16) blocks = (long long)sms * 16;
-    k_permute3_v2<<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<const float4*>(src), dst, n0, n1, n2 / 2, s0,
-                                                    s1, cs);
+    k_permute3_v2<<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<const float4*>(src), dst, (unsigned)n0,
+                                                    (unsigned)n1, (unsigned)(n2 / 2), s0, s1, cs);
   } else {
     const long long total = n0 * n1 * n2;
     long long blocks = (total + 255) / 256;
     if (blocks > (long long)sms * 16) blocks = (long long)sms * 16;
-    k_permute3<<<(unsigned)blocks, 256, 0, st>>>(src, dst, n0, n1, n2, s0, s1, cs);
+    k_permute3<<<(unsigned)blocks, 256, 0, st>>>(src, dst, (unsigned)n0, (unsigned)n1, (unsigned)n2, s0, s1, cs);
   }
   return cudaGetLastError();
 }

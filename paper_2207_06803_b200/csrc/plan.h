@@ -6,13 +6,14 @@
 #include "fourstep.h"
 #include "gpass.h"
 #include "jit.h"
+#include "direct_tc.h"
 #include "l2pass.h"
 #include "passes.h"
 #include "registry.h"
 
 namespace fftc {
 
-enum PlanKind : int { KIND_COPY = 0, KIND_FUSED = 1, KIND_GENERIC = 2, KIND_FOURSTEP = 3, KIND_DIST = 4, KIND_PASSES = 5, KIND_L2 = 6, KIND_GPASS = 7, KIND_JIT = 8 };
+enum PlanKind : int { KIND_COPY = 0, KIND_FUSED = 1, KIND_GENERIC = 2, KIND_FOURSTEP = 3, KIND_DIST = 4, KIND_PASSES = 5, KIND_L2 = 6, KIND_GPASS = 7, KIND_JIT = 8, KIND_DIRECT = 9 };
 
 struct DistState;  // dist.cu
 
@@ -55,6 +56,8 @@ struct fftc_plan {
   const fftc::JitKernel* jk = nullptr;
   int jit_R[32] = {};
   int jit_S = 0;
+  // direct DFT on tensor cores (opt-in): G_hi | G_lo image
+  float* d_direct = nullptr;
   // host-buffer execution
   fftc::HostStage* hs = nullptr;
   // distributed six-step
