@@ -97,8 +97,11 @@ __device__ __forceinline__ void tma_store_2d(const void* tmap, const void* src, 
 }
 
 // One CTA = 4 warps; tile = 128 transforms x 2N floats; persistent over tiles.
-// Shared memory: A (tile, TF32 hi in place, then the output staging) | A_lo | G_hi | G_lo,
-// each [2N/32 atoms][rows][128 B] with the 128-byte swizzle.
+// Shared memory: X[kStages] (input tile -> TF32 hi in place -> output staging) | A_lo | G_hi | G_lo,
+// each [2N/32 atoms][rows][128 B] with the 128-byte swizzle.  The TMA load of tile i + kStages-1
+// is in flight while tile i is split, multiplied and stored.
+constexpr int kStages = 3;
+
 template <int N>
 __global__ void __launch_bounds__(128, 1)
     k_direct_tc(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout,
@@ -110,20 +113,29 @@ __global__ void __launch_bounds__(128, 1)
   constexpr uint32_t TMEM_COLS = N2 < 32 ? 32 : N2;
   extern __shared__ __align__(1024) unsigned char smraw[];
   unsigned char* base = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);
-  float* A = reinterpret_cast<float*>(base);
-  float* Alo = reinterpret_cast<float*>(base + A_BYTES);
-  unsigned char* G = base + 2 * A_BYTES;  // G_hi then G_lo
-  __shared__ __align__(8) uint64_t bar_g, bar_full, bar_mma;
+  float* Alo = reinterpret_cast<float*>(base + kStages * A_BYTES);
+  unsigned char* G = base + (kStages + 1) * A_BYTES;  // G_hi then G_lo
+  __shared__ __align__(8) uint64_t bar_g, bar_full[kStages], bar_mma;
   __shared__ uint32_t s_tmem;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long T = (batch + kTileM - 1) / kTileM;
+  auto tile_of = [&](long long i) { return (long long)blockIdx.x + i * gridDim.x; };
+  auto issue = [&](long long i) {  // TMA load of this CTA's i-th tile into stage i % kStages
+    const long long t = tile_of(i);
+    if (t >= T) return;
+    unsigned char* X = base + (i % kStages) * A_BYTES;
+    mbar_arrive_expect_tx(&bar_full[i % kStages], A_BYTES);
+    for (int a = 0; a < ATOMS; ++a) tma_load_2d(X + a * (kTileM * 128), &tin, a * 32, (int)(t * kTileM), &bar_full[i % kStages]);
+  };
 
   if (threadIdx.x == 0) {
     mbar_init(&bar_g, 1);
-    mbar_init(&bar_full, 1);
+    for (int s = 0; s < kStages; ++s) mbar_init(&bar_full[s], 1);
     mbar_init(&bar_mma, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     mbar_arrive_expect_tx(&bar_g, 2 * G_BYTES);
     bulk_g2s(G, g_img, 2 * G_BYTES, &bar_g);
+    for (int i = 0; i < kStages - 1; ++i) issue(i);
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
@@ -134,29 +146,26 @@ __global__ void __launch_bounds__(128, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = s_tmem;
-  const long long T = (batch + kTileM - 1) / kTileM;
   constexpr uint32_t idesc = instr_desc<N2>();
-  const uint32_t sA = smem_u32(A), sAlo = smem_u32(Alo), sGhi = smem_u32(G), sGlo = smem_u32(G + G_BYTES);
+  const uint32_t sAlo = smem_u32(Alo), sGhi = smem_u32(G), sGlo = smem_u32(G + G_BYTES);
   mbar_wait(&bar_g, 0);
-  uint32_t ph = 0;
-  for (long long t = blockIdx.x; t < T; t += gridDim.x, ph ^= 1) {
-    const int row0 = (int)(t * kTileM);
-    if (threadIdx.x == 0) {
-      bulk_wait_read0();  // the previous tile's store has finished reading A
-      mbar_arrive_expect_tx(&bar_full, A_BYTES);
-      for (int a = 0; a < ATOMS; ++a) tma_load_2d(base + a * (kTileM * 128), &tin, a * 32, row0, &bar_full);
-    }
-    mbar_wait(&bar_full, ph);
-    // hi / lo split in place (elementwise: the swizzled position is the same in both buffers)
+  for (long long i = 0; tile_of(i) < T; ++i) {
+    const long long t = tile_of(i);
+    const int s = (int)(i % kStages);
+    unsigned char* X = base + s * A_BYTES;
+    const uint32_t sX = smem_u32(X);
+    mbar_wait(&bar_full[s], (uint32_t)((i / kStages) & 1));
+    // hi / lo split (elementwise: the swizzled position is the same in both buffers)
     {
-      float4* a4 = reinterpret_cast<float4*>(A);
+      float4* a4 = reinterpret_cast<float4*>(X);
       float4* l4 = reinterpret_cast<float4*>(Alo);
-      for (int i = threadIdx.x; i < (int)(A_BYTES / 16); i += 128) {
-        float4 v = a4[i];
+#pragma unroll 4
+      for (int q = threadIdx.x; q < (int)(A_BYTES / 16); q += 128) {
+        float4 v = a4[q];
         const float hx = __uint_as_float(to_tf32(v.x)), hy = __uint_as_float(to_tf32(v.y));
         const float hz = __uint_as_float(to_tf32(v.z)), hw = __uint_as_float(to_tf32(v.w));
-        l4[i] = make_float4(v.x - hx, v.y - hy, v.z - hz, v.w - hw);
-        a4[i] = make_float4(hx, hy, hz, hw);
+        l4[q] = make_float4(v.x - hx, v.y - hy, v.z - hz, v.w - hw);
+        a4[q] = make_float4(hx, hy, hz, hw);
       }
     }
     fence_proxy_async_smem();
@@ -167,26 +176,27 @@ __global__ void __launch_bounds__(128, 1)
       for (int k = 0; k < N2 / 8; ++k) {
         const uint32_t off_a = (uint32_t)(k >> 2) * (kTileM * 128) + (uint32_t)(k & 3) * 32;
         const uint32_t off_g = (uint32_t)(k >> 2) * (N2 * 128) + (uint32_t)(k & 3) * 32;
-        mma_tf32(tmem, umma_desc(sA + off_a), umma_desc(sGhi + off_g), idesc, k > 0);
-        mma_tf32(tmem, umma_desc(sA + off_a), umma_desc(sGlo + off_g), idesc, 1);
+        mma_tf32(tmem, umma_desc(sX + off_a), umma_desc(sGhi + off_g), idesc, k > 0);
+        mma_tf32(tmem, umma_desc(sX + off_a), umma_desc(sGlo + off_g), idesc, 1);
         mma_tf32(tmem, umma_desc(sAlo + off_a), umma_desc(sGhi + off_g), idesc, 1);
       }
       mma_commit(&bar_mma);
+      // refill the stage the previous tile used, once its store has finished reading it
+      bulk_wait_read0();
+      issue(i + kStages - 1);
     }
-    mbar_wait(&bar_mma, ph);
+    mbar_wait(&bar_mma, (uint32_t)(i & 1));
     tc_fence_after();
-    // epilogue: warp w owns accumulator lanes (tile rows) 32w..32w+31; row r -> swizzled A
+    // epilogue: warp w owns accumulator lanes (tile rows) 32w..32w+31; row r -> swizzled X
     {
       const int r = warp * 32 + lane;
-      float* rowbase = A;
       for (int c0 = 0; c0 < N2; c0 += 32) {
         uint32_t v[32];
         tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
         const int a = c0 / 32;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {  // 16-byte chunks of the 128-byte row segment
-          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<unsigned char*>(rowbase) + a * (kTileM * 128) +
-                                                  r * 128 + ((q ^ (r & 7)) << 4));
+          float4* dst = reinterpret_cast<float4*>(X + a * (kTileM * 128) + r * 128 + ((q ^ (r & 7)) << 4));
           *dst = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]), __uint_as_float(v[4 * q + 2]),
                              __uint_as_float(v[4 * q + 3]));
         }
@@ -196,7 +206,7 @@ __global__ void __launch_bounds__(128, 1)
     fence_proxy_async_smem();
     __syncthreads();
     if (threadIdx.x == 0) {
-      for (int a = 0; a < ATOMS; ++a) tma_store_2d(&tout, base + a * (kTileM * 128), a * 32, row0);
+      for (int a = 0; a < ATOMS; ++a) tma_store_2d(&tout, X + a * (kTileM * 128), a * 32, (int)(t * kTileM));
       bulk_commit();
     }
   }
@@ -235,7 +245,7 @@ bool map_rows(CUtensorMap* m, const void* base, int N, long long batch) {
 
 template <int N>
 cudaError_t launch_direct(const float2* in, float2* out, const float* g_img, long long batch, cudaStream_t st) {
-  constexpr size_t smem = (size_t)2 * kTileM * 2 * N * 4 + (size_t)2 * (2 * N) * (2 * N) * 4 + 1024;
+  constexpr size_t smem = (size_t)(kStages + 1) * kTileM * 2 * N * 4 + (size_t)2 * (2 * N) * (2 * N) * 4 + 1024;
   auto kern = k_direct_tc<N>;
   static int grid_max = 0;
   if (!grid_max) {
