@@ -100,9 +100,7 @@ __device__ __forceinline__ void tma_store_2d(const void* tmap, const void* src, 
 // Shared memory: X[kStages] (input tile -> TF32 hi in place -> output staging) | A_lo | G_hi | G_lo,
 // each [2N/32 atoms][rows][128 B] with the 128-byte swizzle.  The TMA load of tile i + kStages-1
 // is in flight while tile i is split, multiplied and stored.
-constexpr int kStages = 3;
-
-template <int N>
+template <int N, int kStages>
 __global__ void __launch_bounds__(128, 1)
     k_direct_tc(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout,
                 const float* __restrict__ g_img, long long batch) {
@@ -154,6 +152,10 @@ __global__ void __launch_bounds__(128, 1)
     const int s = (int)(i % kStages);
     unsigned char* X = base + s * A_BYTES;
     const uint32_t sX = smem_u32(X);
+    if (kStages == 1 && threadIdx.x == 0) {  // no prefetch: load this tile now
+      bulk_wait_read0();
+      issue(i);
+    }
     mbar_wait(&bar_full[s], (uint32_t)((i / kStages) & 1));
     // hi / lo split (elementwise: the swizzled position is the same in both buffers)
     {
@@ -182,8 +184,10 @@ __global__ void __launch_bounds__(128, 1)
       }
       mma_commit(&bar_mma);
       // refill the stage the previous tile used, once its store has finished reading it
-      bulk_wait_read0();
-      issue(i + kStages - 1);
+      if (kStages > 1) {
+        bulk_wait_read0();
+        issue(i + kStages - 1);
+      }
     }
     mbar_wait(&bar_mma, (uint32_t)(i & 1));
     tc_fence_after();
@@ -243,26 +247,29 @@ bool map_rows(CUtensorMap* m, const void* base, int N, long long batch) {
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int N>
+template <int N, int S, int PER_SM>
 cudaError_t launch_direct(const float2* in, float2* out, const float* g_img, long long batch, cudaStream_t st) {
-  constexpr size_t smem = (size_t)(kStages + 1) * kTileM * 2 * N * 4 + (size_t)2 * (2 * N) * (2 * N) * 4 + 1024;
-  auto kern = k_direct_tc<N>;
+  constexpr size_t smem = (size_t)(S + 1) * kTileM * 2 * N * 4 + (size_t)2 * (2 * N) * (2 * N) * 4 + 1024;
+  static_assert(PER_SM * smem <= 227 * 1024, "CTAs per SM must fit in shared memory");
+  auto kern = k_direct_tc<N, S>;
   static int grid_max = 0;
   if (!grid_max) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)  // let PER_SM CTAs share an SM
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
-    int dev = 0, sms = 0, per = 0;
+    int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 128, smem);
-    if (e != cudaSuccess) return e;
-    grid_max = sms * (per > 0 ? per : 1);
+    grid_max = PER_SM * sms;
   }
   CUtensorMap ti, to;
   if (!map_rows(&ti, in, N, batch) || !map_rows(&to, out, N, batch)) return cudaErrorInvalidValue;
   const long long T = (batch + kTileM - 1) / kTileM;
   if (T == 0) return cudaSuccess;
-  const unsigned grid = (unsigned)(T < grid_max ? T : grid_max);
+  long long gm = grid_max;
+  if (const char* g = getenv("FFTC_DIRECT_GRID")) gm = atoll(g);  // tuning
+  const unsigned grid = (unsigned)(T < gm ? T : gm);
   kern<<<grid, 128, smem, st>>>(ti, to, g_img, batch);
   return cudaGetLastError();
 }
@@ -318,8 +325,10 @@ float* direct_tables(long long N, int sign, cudaError_t* err) {
 cudaError_t direct_execute(long long N, const float2* in, float2* out, const float* g_img, long long batch,
                            cudaStream_t st) {
   if (batch == 0) return cudaSuccess;
-  if (N == 16) return launch_direct<16>(in, out, g_img, batch, st);
-  if (N == 32) return launch_direct<32>(in, out, g_img, batch, st);
+  // measured on B200 (profiles/r01f): N = 16: 3-stage ring, 2 CTAs/SM (73 KB each) 5.6 TB/s;
+  // N = 32: 3-stage ring, 1 CTA/SM (161 KB) 4.55 TB/s (1 stage x 2 CTAs/SM: 4.1 TB/s)
+  if (N == 16) return launch_direct<16, 3, 2>(in, out, g_img, batch, st);
+  if (N == 32) return launch_direct<32, 3, 1>(in, out, g_img, batch, st);
   return cudaErrorInvalidValue;
 }
 
