@@ -360,7 +360,7 @@ def run_c5(args):
     else:
         nid = None
     lb = args.c5_loopback if world == 1 else 0
-    plan = fftc.Plan.dist(N, -1, nid, rank, lb or world, loopback=bool(lb))
+    plan = fftc.Plan.dist(N, -1, nid, rank, lb or world, loopback=bool(lb), flags=args.c5_flags)
     slab = N // world
     # rank r holds elements [r N/P, (r+1) N/P) of one seeded U[-1,1) vector (generated per slab
     # from a per-rank seed so no rank materialises the whole 8 GiB vector)
@@ -441,6 +441,8 @@ def main():
     ap.add_argument("--c5-n", type=int, default=1 << 30)
     ap.add_argument("--c5-loopback", type=int, default=0,
                     help="one GPU: run the six-step for P virtual ranks (all-to-alls = device copies)")
+    ap.add_argument("--c5-flags", type=int, default=0,
+                    help="six-step options: 1 = transposed output (no all-to-all #3), 2 = fused peer-store exchanges")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--graph", action="store_true", help="also time the step captured in a CUDA graph")
     ap.add_argument("--no-cpu", action="store_true")

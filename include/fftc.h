@@ -206,6 +206,21 @@ fftc_status fftc_dist_get_unique_id(void* id_out);
 fftc_plan* fftc_dist_plan_create(int64_t N, int sign, const void* nccl_id, int rank, int nranks,
                                  int loopback);
 
+/* Options of fftc_dist_plan_create_ex (bit flags):
+ * FFTC_DIST_TRANSPOSED_OUT: drop all-to-all #3 -- rank p's out holds
+ *   out[k1*Mp + jl] = X[p*Mp + jl + M*k1] (k1 < K, jl < Mp = M/P), the
+ *   natural output of the last local DFT.
+ * FFTC_DIST_PEER_STORES: fuse the exchanges into the kernels around them:
+ *   the pack kernel stores each chunk straight into the receiving rank's
+ *   buffer and the DFT_M kernel's epilogue does the same for exchange #2
+ *   (P2P stores over NVLink into buffers mapped by CUDA IPC, handles
+ *   all-gathered over NCCL at create; a 1-int NCCL all-reduce orders each
+ *   exchange).  nranks <= 8.                                               */
+#define FFTC_DIST_TRANSPOSED_OUT 1
+#define FFTC_DIST_PEER_STORES 2
+fftc_plan* fftc_dist_plan_create_ex(int64_t N, int sign, const void* nccl_id, int rank, int nranks,
+                                    int loopback, int flags);
+
 /* fftc_execute on a distributed plan: in / out are this rank's
  * N/nranks-element natural-order slabs (device); in loopback mode the whole
  * N-element vectors.  Enqueues 4-5 kernels and 3 all-to-alls per call. */

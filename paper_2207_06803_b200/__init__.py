@@ -62,6 +62,7 @@ def load(path: str = LIB_PATH):
         "fftc_plan_split": ([i64, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)], i32),
         "fftc_dist_get_unique_id": ([vp], i32),
         "fftc_dist_plan_create": ([i64, i32, vp, i32, i32, i32], vp),
+        "fftc_dist_plan_create_ex": ([i64, i32, vp, i32, i32, i32, i32], vp),
         "fftc_dist_split": ([i64, i32, ctypes.POINTER(ctypes.c_int64)], i32),
         "fftc_candidates": ([i64, ctypes.POINTER(ctypes.c_char_p), i32], i32),
         "fftc_plan_passes": ([i64, ctypes.POINTER(ctypes.c_int), i32], i32),
@@ -198,10 +199,14 @@ def fftc_dist_get_unique_id() -> bytes:
     return buf.raw
 
 
+FFTC_DIST_TRANSPOSED_OUT = 1
+FFTC_DIST_PEER_STORES = 2
+
+
 def fftc_dist_plan_create(N: int, sign: int, nccl_id: bytes | None, rank: int, nranks: int,
-                          loopback: bool = False) -> int:
+                          loopback: bool = False, flags: int = 0) -> int:
     idbuf = ctypes.create_string_buffer(nccl_id, FFTC_NCCL_ID_BYTES) if nccl_id else None
-    return load().fftc_dist_plan_create(N, sign, idbuf, rank, nranks, int(loopback)) or 0
+    return load().fftc_dist_plan_create_ex(N, sign, idbuf, rank, nranks, int(loopback), flags) or 0
 
 
 # ---------------------------------------------------------------- convenience wrapper
@@ -240,8 +245,9 @@ class Plan:
         return cls(N, batch, sign, _handle=h)
 
     @classmethod
-    def dist(cls, N: int, sign: int, nccl_id: bytes | None, rank: int, nranks: int, loopback: bool = False):
-        h = fftc_dist_plan_create(N, sign, nccl_id, rank, nranks, loopback)
+    def dist(cls, N: int, sign: int, nccl_id: bytes | None, rank: int, nranks: int, loopback: bool = False,
+             flags: int = 0):
+        h = fftc_dist_plan_create(N, sign, nccl_id, rank, nranks, loopback, flags)
         if not h:
             raise FFTCError(fftc_last_error(), "fftc_dist_plan_create(N=%d, P=%d)" % (N, nranks))
         p = cls.__new__(cls)

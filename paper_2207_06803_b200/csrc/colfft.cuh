@@ -9,6 +9,8 @@
 // Geometry (runtime, ColGeom): column c = grp * G + ci (ci < G = tiles * C);
 //   input  element i : in  + grp*in_g  + ci + i*in_s
 //   output element k : out + grp*out_g + ci*out_c + (k >> ocl)*out_cs + (k & omask)*out_s
+//   (or, with npeer > 0, peer[k >> ocl] + grp*out_g + ci*out_c + (k & omask)*out_s: the
+//    chunk goes straight into another rank's receive buffer over NVLink)
 //   optional twiddle : y_k *= w_T^{((ci >> tw_shift) + tw_off) * k}   (T-point root,
 //                      read as A[e mod 4096] * B[e div 4096] from two fp32 tables)
 // OUT_T = false: the last stage stores HBM directly (lanes walk columns; needs out_c = 1).
@@ -81,8 +83,9 @@ __global__ void __launch_bounds__(P::THREADS, MINB)
     float2* go = out + grp * g.out_g + ci * g.out_c;
     run_stages<P, true, true>(sm, f, lt, true, tw, load, [&](int k, float2 v, int r) {
       v = twiddle(k, v, r);
-      __stcs(go + ((long long)k >> g.ocl) * g.out_cs + ((long long)k & omask) * g.out_s,
-             make_float2(v.x, csign_out * v.y));
+      float2* dst = g.npeer ? reinterpret_cast<float2*>(g.peer[k >> g.ocl]) + grp * g.out_g + ci * g.out_c
+                            : go + ((long long)k >> g.ocl) * g.out_cs;
+      __stcs(dst + ((long long)k & omask) * g.out_s, make_float2(v.x, csign_out * v.y));
     });
   } else {
     // last stage: twiddled values back into the exchange buffer, then a store walking k
@@ -98,8 +101,9 @@ __global__ void __launch_bounds__(P::THREADS, MINB)
       const int e = threadIdx.x + n * P::THREADS;
       const int k = e % L, cc = e / L;
       const float2 v = sm[P::sidx(cc, k)];
-      __stcs(go + (long long)(ci0 + cc) * g.out_c + ((long long)k >> g.ocl) * g.out_cs +
-                 ((long long)k & omask) * g.out_s,
+      float2* dst = g.npeer ? reinterpret_cast<float2*>(g.peer[k >> g.ocl]) + grp * g.out_g
+                            : go + ((long long)k >> g.ocl) * g.out_cs;
+      __stcs(dst + (long long)(ci0 + cc) * g.out_c + ((long long)k & omask) * g.out_s,
              make_float2(v.x, csign_out * v.y));
     });
   }

@@ -15,6 +15,11 @@ struct ColGeom {
   int tw;            // apply the twiddle
   int tw_shift;      // twiddle column index = (ci >> tw_shift) + tw_off
   long long tw_off;
+  // Peer destinations (distributed six-step, fused exchange): when npeer > 0 the chunk
+  // index (k >> ocl) selects the base pointer peer[k >> ocl] (another rank's receive
+  // buffer, mapped over NVLink) instead of out + (k >> ocl) * out_cs.
+  int npeer;
+  unsigned long long peer[8];
 };
 
 }  // namespace fftc

@@ -45,6 +45,14 @@ struct DistState {
   float2 *send = nullptr, *recv = nullptr, *work = nullptr;  // nloc * N/P each
   ncclComm_t comm = nullptr;
   int launches = 0;
+  int flags = 0;                 // FFTC_DIST_TRANSPOSED_OUT | FFTC_DIST_PEER_STORES
+  // peer-store exchange: a second receive buffer (exchange #2) and every rank's receive
+  // buffers mapped into this process (CUDA IPC over NVLink; in loopback, this GPU's slabs)
+  float2* recv2 = nullptr;
+  float2* peerA[8] = {};         // rank q's receive buffer of exchange #1
+  float2* peerB[8] = {};         // rank q's receive buffer of exchange #2
+  bool ipc_opened[8] = {};
+  int* bar = nullptr;            // 1-int NCCL barrier buffer
 };
 
 namespace {
@@ -71,6 +79,36 @@ __global__ void k_permute3_v2(const float4* __restrict__ src, float2* __restrict
     float4 a = __ldcs(src + t);
     __stcs(reinterpret_cast<float4*>(dst + i0 * s0 + i1 * s1 + i2), make_float4(a.x, csign * a.y, a.z, csign * a.w));
   }
+}
+
+// Fused pack + exchange #1: dst_{i1}[i0*s0 + i2] = src[(i0*n1 + i1)*n2 + i2], the destination
+// base chosen per i1 (= the receiving rank) from a table of peer pointers.
+struct PeerTable {
+  float2* p[8];
+};
+__global__ void k_permute3_peer(const float2* __restrict__ src, PeerTable dst, unsigned n0, unsigned n1, unsigned n2,
+                                long long s0, float csign) {
+  const unsigned total = n0 * n1 * n2;
+  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const unsigned r = t / n2, i2 = t - r * n2;
+    const unsigned i0 = r / n1, i1 = r - i0 * n1;
+    float2 a = __ldcs(src + t);
+    __stcs(dst.p[i1] + i0 * s0 + i2, make_float2(a.x, csign * a.y));
+  }
+}
+
+cudaError_t permute3_peer(const float2* src, const PeerTable& dst, long long n0, long long n1, long long n2,
+                          long long s0, int conj, cudaStream_t st) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (n0 * n1 * n2 >= (1LL << 32) || n1 > 8) return cudaErrorInvalidValue;
+  const long long total = n0 * n1 * n2;
+  long long blocks = (total + 255) / 256;
+  if (blocks > (long long)sms * 16) blocks = (long long)sms * 16;
+  k_permute3_peer<<<(unsigned)blocks, 256, 0, st>>>(src, dst, (unsigned)n0, (unsigned)n1, (unsigned)n2, s0,
+                                                    conj ? -1.f : 1.f);
+  return cudaGetLastError();
 }
 
 cudaError_t permute3(const float2* src, float2* dst, long long n0, long long n1, long long n2, long long s0,
@@ -163,6 +201,17 @@ cudaError_t all_to_all(DistState* d, cudaStream_t st, fftc_status* ns) {
                          cudaMemcpyDeviceToDevice, st);
 }
 
+// Cross-rank barrier on the stream (a 1-int NCCL all-reduce): every rank's earlier kernels,
+// including their stores into this rank's buffers, are complete when it returns.
+cudaError_t barrier(DistState* d, cudaStream_t st, fftc_status* ns) {
+  if (d->loopback || d->P == 1) return cudaSuccess;
+  if (ncclAllReduce(d->bar, d->bar, 1, ncclInt, ncclSum, d->comm, st) != ncclSuccess) {
+    *ns = FFTC_ERROR_NCCL;
+    return cudaErrorUnknown;
+  }
+  return cudaSuccess;
+}
+
 }  // namespace
 
 fftc_status dist_execute(DistState* d, const void* in, void* out, cudaStream_t st) {
@@ -177,12 +226,30 @@ fftc_status dist_execute(DistState* d, const void* in, void* out, cudaStream_t s
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return FFTC_ERROR_CUDA;
   const int64_t M = d->M, K = d->K, Mp = d->Mp, Kp = d->Kp, P = d->P;
-  // 1. pack: src x_p viewed as [ql][d][rl] (Mp, P, Kp) -> send[d][ql][rl]
-  for (int p = 0; p < d->nloc && e == cudaSuccess; ++p)
-    e = permute3(x + p * slab, d->send + p * slab, Mp, P, Kp, Kp, Mp * Kp, conj, st);
-  // 2. a2a #1
-  if (e == cudaSuccess) e = all_to_all(d, st, &ns);
+  const bool peer = (d->flags & FFTC_DIST_PEER_STORES) != 0;
+  const bool tout = (d->flags & FFTC_DIST_TRANSPOSED_OUT) != 0;
+  const int64_t chunk = Mp * Kp;
+  float2* recvA = d->recv;                 // exchange #1 lands here
+  float2* recvB = peer ? d->recv2 : d->recv;  // exchange #2 lands here
+  if (peer) {
+    // 1+2. pack fused with exchange #1: x_p[ql][d][rl] -> rank d's recvA[p][ql][rl] (NVLink stores)
+    e = barrier(d, st, &ns);  // every rank is done reading its receive buffers (previous call)
+    for (int p = 0; p < d->nloc && e == cudaSuccess; ++p) {
+      const int prank = d->loopback ? p : d->rank;
+      PeerTable t{};
+      for (int q = 0; q < P; ++q) t.p[q] = d->peerA[q] + prank * chunk;
+      e = permute3_peer(x + p * slab, t, Mp, P, Kp, Kp, conj, st);
+    }
+    if (e == cudaSuccess) e = barrier(d, st, &ns);
+  } else {
+    // 1. pack: src x_p viewed as [ql][d][rl] (Mp, P, Kp) -> send[d][ql][rl]
+    for (int p = 0; p < d->nloc && e == cudaSuccess; ++p)
+      e = permute3(x + p * slab, d->send + p * slab, Mp, P, Kp, Kp, Mp * Kp, conj, st);
+    // 2. a2a #1
+    if (e == cudaSuccess) e = all_to_all(d, st, &ns);
+  }
   // 3. DFT_M down columns rl of B[q][rl] (stride Kp), twiddle w_N^{(p Kp + rl) j}, transposed out
+  //    (peer mode: chunk j / Mp goes straight to that rank's recvB[p] -- exchange #2 fused)
   for (int p = 0; p < d->nloc && e == cudaSuccess; ++p) {
     const int prank = d->loopback ? p : d->rank;
     ColGeom g{};
@@ -197,12 +264,19 @@ fftc_status dist_execute(DistState* d, const void* in, void* out, cudaStream_t s
     g.tw = 1;
     g.tw_shift = 0;
     g.tw_off = (long long)prank * Kp;
-    e = d->cM->launch_t(d->recv + p * slab, d->send + p * slab, d->twM, d->twA_N, d->twB_N, g, 1, 0, 0, st);
+    if (peer) {
+      g.npeer = (int)P;
+      for (int q = 0; q < P; ++q) g.peer[q] = (unsigned long long)(d->peerB[q] + prank * chunk);
+    }
+    e = d->cM->launch_t(recvA + p * slab, d->send + p * slab, d->twM, d->twA_N, d->twB_N, g, 1, 0, 0, st);
   }
   // 4. a2a #2
-  if (e == cudaSuccess) e = all_to_all(d, st, &ns);
+  if (e == cudaSuccess) e = peer ? barrier(d, st, &ns) : all_to_all(d, st, &ns);
   // 5. DFT_K down columns jl of V[r][jl] (stride Mp) -> send[k1][jl]
+  //    (transposed-output mode: straight into out, with the inverse's output conjugation)
   for (int p = 0; p < d->nloc && e == cudaSuccess; ++p) {
+    float2* kout = tout ? X + p * slab : d->send + p * slab;
+    const int cj = tout ? conj : 0;
     if (d->K2 == 1) {
       ColGeom g{};
       g.tiles = (int)(Mp / d->cK1->cols);
@@ -210,7 +284,7 @@ fftc_status dist_execute(DistState* d, const void* in, void* out, cudaStream_t s
       g.out_c = 1;
       g.out_s = Mp;
       g.ocl = 62;
-      e = d->cK1->launch(d->recv + p * slab, d->send + p * slab, d->twK1, nullptr, nullptr, g, 1, 0, 0, st);
+      e = d->cK1->launch(recvB + p * slab, kout, d->twK1, nullptr, nullptr, g, 1, 0, cj, st);
     } else {
       const int64_t K1 = d->K1, K2 = d->K2;
       // pass A: columns (b, jl) -> c = b Mp + jl, DFT_K1 over a (stride K2 Mp), twiddle w_K^{b ja}
@@ -222,7 +296,7 @@ fftc_status dist_execute(DistState* d, const void* in, void* out, cudaStream_t s
       a.ocl = 62;
       a.tw = 1;
       a.tw_shift = ilog2ll(Mp);
-      e = d->cK1->launch(d->recv + p * slab, d->work + p * slab, d->twK1, d->twA_K, d->twB_K, a, 1, 0, 0, st);
+      e = d->cK1->launch(recvB + p * slab, d->work + p * slab, d->twK1, d->twA_K, d->twB_K, a, 1, 0, 0, st);
       // pass B: groups ja, columns jl, DFT_K2 over b (stride Mp), out X[(ja + K1 kb) Mp + jl]
       ColGeom b{};
       b.tiles = (int)(Mp / d->cK2->cols);
@@ -232,15 +306,16 @@ fftc_status dist_execute(DistState* d, const void* in, void* out, cudaStream_t s
       b.out_c = 1;
       b.out_s = K1 * Mp;
       b.ocl = 62;
-      if (e == cudaSuccess)
-        e = d->cK2->launch(d->work + p * slab, d->send + p * slab, d->twK2, nullptr, nullptr, b, K1, 0, 0, st);
+      if (e == cudaSuccess) e = d->cK2->launch(d->work + p * slab, kout, d->twK2, nullptr, nullptr, b, K1, 0, cj, st);
     }
   }
-  // 6. a2a #3
-  if (e == cudaSuccess) e = all_to_all(d, st, &ns);
-  // 7. unpack: recv viewed as [s][k1l][jl] (P, Kp, Mp) -> X_p[k1l M + s Mp + jl]
-  for (int p = 0; p < d->nloc && e == cudaSuccess; ++p)
-    e = permute3(d->recv + p * slab, X + p * slab, P, Kp, Mp, Mp, M, conj, st);
+  if (!tout) {
+    // 6. a2a #3
+    if (e == cudaSuccess) e = all_to_all(d, st, &ns);
+    // 7. unpack: recv viewed as [s][k1l][jl] (P, Kp, Mp) -> X_p[k1l M + s Mp + jl]
+    for (int p = 0; p < d->nloc && e == cudaSuccess; ++p)
+      e = permute3(d->recv + p * slab, X + p * slab, P, Kp, Mp, Mp, M, conj, st);
+  }
   (void)K;
   if (ns != FFTC_SUCCESS) return ns;
   return e == cudaSuccess ? FFTC_SUCCESS : FFTC_ERROR_CUDA;
@@ -255,8 +330,16 @@ void dist_destroy(DistState* d) {
   cudaFree(d->twB_N);
   cudaFree(d->twA_K);
   cudaFree(d->twB_K);
+  for (int q = 0; q < 8; ++q) {
+    if (d->ipc_opened[q]) {
+      cudaIpcCloseMemHandle(d->peerA[q]);
+      cudaIpcCloseMemHandle(d->peerB[q]);
+    }
+  }
   cudaFree(d->send);
   cudaFree(d->recv);
+  cudaFree(d->recv2);
+  cudaFree(d->bar);
   cudaFree(d->work);
   if (d->comm) ncclCommDestroy(d->comm);
   delete d;
@@ -268,9 +351,12 @@ int dist_describe(const DistState* d, char* buf, size_t len) {
   if (!d) return -1;
   return snprintf(buf, len,
                   "kind=dist N=%lld P=%d rank=%d sign=%d M=%lld K=%lld K1=%lld K2=%lld Mp=%lld Kp=%lld loopback=%d "
-                  "launches=%d a2a=3 chunk_bytes=%lld",
+                  "launches=%d a2a=%d exchange=%s output=%s chunk_bytes=%lld",
                   (long long)d->N, d->P, d->rank, d->sign, (long long)d->M, (long long)d->K, (long long)d->K1,
                   (long long)d->K2, (long long)d->Mp, (long long)d->Kp, (int)d->loopback, d->launches,
+                  (d->flags & FFTC_DIST_TRANSPOSED_OUT) ? 2 : 3,
+                  (d->flags & FFTC_DIST_PEER_STORES) ? "peer-stores(#1,#2 fused)" : "nccl",
+                  (d->flags & FFTC_DIST_TRANSPOSED_OUT) ? "transposed" : "natural",
                   (long long)(d->Mp * d->Kp * (int64_t)sizeof(float2)));
 }
 
@@ -301,8 +387,16 @@ extern "C" fftc_status fftc_dist_get_unique_id(void* id_out) {
   return FFTC_SUCCESS;
 }
 
+extern "C" fftc_plan* fftc_dist_plan_create_ex(int64_t N, int sign, const void* nccl_id, int rank, int nranks,
+                                               int loopback, int flags);
+
 extern "C" fftc_plan* fftc_dist_plan_create(int64_t N, int sign, const void* nccl_id, int rank, int nranks,
                                             int loopback) {
+  return fftc_dist_plan_create_ex(N, sign, nccl_id, rank, nranks, loopback, 0);
+}
+
+extern "C" fftc_plan* fftc_dist_plan_create_ex(int64_t N, int sign, const void* nccl_id, int rank, int nranks,
+                                               int loopback, int flags) {
   auto fail = [&](fftc_status s, DistState* d) -> fftc_plan* {
     dist_destroy(d);
     fftc_set_last_error(s);
@@ -311,9 +405,11 @@ extern "C" fftc_plan* fftc_dist_plan_create(int64_t N, int sign, const void* ncc
   if (N < 2 || (sign != -1 && sign != 1) || nranks < 1 || (!loopback && (rank < 0 || rank >= nranks)))
     return fail(FFTC_ERROR_INVALID_VALUE, nullptr);
   if (!loopback && nranks > 1 && !nccl_id) return fail(FFTC_ERROR_INVALID_VALUE, nullptr);
+  if (flags & ~(FFTC_DIST_TRANSPOSED_OUT | FFTC_DIST_PEER_STORES)) return fail(FFTC_ERROR_INVALID_VALUE, nullptr);
+  if ((flags & FFTC_DIST_PEER_STORES) && nranks > 8) return fail(FFTC_ERROR_UNSUPPORTED_SIZE, nullptr);
   // One rank without loopback: every all-to-all is the identity, so the transform is
   // the single-GPU plan (multi-pass / four-step / fused) -- no copies, no extra passes.
-  if (nranks == 1 && !loopback && !getenv("FFTC_DIST_SIXSTEP")) return fftc_plan_create(N, 1, sign);
+  if (nranks == 1 && !loopback && !flags && !getenv("FFTC_DIST_SIXSTEP")) return fftc_plan_create(N, 1, sign);
   int dev = 0;
   fftc_status ds = fftc_check_device(&dev);
   if (ds != FFTC_SUCCESS) return fail(ds, nullptr);
@@ -324,6 +420,7 @@ extern "C" fftc_plan* fftc_dist_plan_create(int64_t N, int sign, const void* ncc
   d->sign = sign;
   d->loopback = loopback != 0;
   d->nloc = d->loopback ? nranks : 1;
+  d->flags = flags;
   if (!dist_split(N, nranks, d)) return fail(FFTC_ERROR_UNSUPPORTED_SIZE, d);
   cudaError_t err = cudaSuccess;
   d->twM = upload_stage_table(d->M, d->cM->R, d->cM->S, &err);
@@ -339,12 +436,58 @@ extern "C" fftc_plan* fftc_dist_plan_create(int64_t N, int sign, const void* ncc
   if (err == cudaSuccess && d->cK2) err = cudaMalloc(&d->work, bytes);
   if (err != cudaSuccess)
     return fail(err == cudaErrorMemoryAllocation ? FFTC_ERROR_OUT_OF_MEMORY : FFTC_ERROR_CUDA, d);
+  const bool peer = (flags & FFTC_DIST_PEER_STORES) != 0;
+  if (err == cudaSuccess && peer) err = cudaMalloc(&d->recv2, bytes);
+  if (err == cudaSuccess && peer) err = cudaMalloc(&d->bar, 256);
+  if (err == cudaSuccess && peer) err = cudaMemset(d->bar, 0, 256);
+  if (err != cudaSuccess)
+    return fail(err == cudaErrorMemoryAllocation ? FFTC_ERROR_OUT_OF_MEMORY : FFTC_ERROR_CUDA, d);
   if (!d->loopback && nranks > 1) {
     ncclUniqueId id;
     memcpy(&id, nccl_id, sizeof(id));
     if (ncclCommInitRank(&d->comm, nranks, id, rank) != ncclSuccess) return fail(FFTC_ERROR_NCCL, d);
   }
-  d->launches = d->nloc * (d->cK2 ? 5 : 4);
+  const int64_t slab = N / nranks;
+  if (peer && (d->loopback || nranks == 1)) {
+    for (int q = 0; q < nranks; ++q) {  // the virtual ranks' slabs on this GPU
+      d->peerA[q] = d->recv + q * slab;
+      d->peerB[q] = d->recv2 + q * slab;
+    }
+  } else if (peer) {
+    // map every rank's receive buffers: CUDA IPC handles all-gathered over NCCL
+    cudaIpcMemHandle_t h[2];
+    if (cudaIpcGetMemHandle(&h[0], d->recv) != cudaSuccess || cudaIpcGetMemHandle(&h[1], d->recv2) != cudaSuccess)
+      return fail(FFTC_ERROR_CUDA, d);
+    const size_t hb = sizeof(h);
+    char* dh = nullptr;
+    std::vector<char> all((size_t)nranks * hb);
+    cudaStream_t cs = nullptr;
+    bool ok = cudaMalloc(&dh, (size_t)(nranks + 1) * hb) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaMemcpy(dh + (size_t)nranks * hb, h, hb, cudaMemcpyHostToDevice) == cudaSuccess &&
+              ncclAllGather(dh + (size_t)nranks * hb, dh, hb, ncclChar, d->comm, cs) == ncclSuccess &&
+              cudaStreamSynchronize(cs) == cudaSuccess &&
+              cudaMemcpy(all.data(), dh, all.size(), cudaMemcpyDeviceToHost) == cudaSuccess;
+    if (cs) cudaStreamDestroy(cs);
+    cudaFree(dh);
+    for (int q = 0; ok && q < nranks; ++q) {
+      if (q == rank) {
+        d->peerA[q] = d->recv;
+        d->peerB[q] = d->recv2;
+        continue;
+      }
+      cudaIpcMemHandle_t hq[2];
+      memcpy(hq, all.data() + (size_t)q * hb, hb);
+      void *pa = nullptr, *pb = nullptr;
+      ok = cudaIpcOpenMemHandle(&pa, hq[0], cudaIpcMemLazyEnablePeerAccess) == cudaSuccess &&
+           cudaIpcOpenMemHandle(&pb, hq[1], cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
+      d->peerA[q] = (float2*)pa;
+      d->peerB[q] = (float2*)pb;
+      d->ipc_opened[q] = ok;
+    }
+    if (!ok) return fail(FFTC_ERROR_CUDA, d);
+  }
+  d->launches = d->nloc * (d->cK2 ? 5 : 4) - ((flags & FFTC_DIST_TRANSPOSED_OUT) ? d->nloc : 0);
   fftc_plan* p = new fftc_plan();
   p->N = N;
   p->batch = 1;

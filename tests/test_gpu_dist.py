@@ -17,10 +17,10 @@ import paper_2207_06803_b200 as fftc  # noqa: E402
 pytestmark = pytest.mark.gpu
 
 
-def run_dist(x, sign, P, loopback=True):
+def run_dist(x, sign, P, loopback=True, flags=0):
     N = x.size
     d = torch.from_numpy(np.ascontiguousarray(x)).cuda()
-    p = fftc.Plan.dist(N, sign, None, 0, P, loopback=loopback)
+    p = fftc.Plan.dist(N, sign, None, 0, P, loopback=loopback, flags=flags)
     try:
         y = torch.empty_like(d)
         p.execute(d, y)
@@ -102,3 +102,36 @@ def test_config5_loopback_2p30():
     num = torch.linalg.vector_norm(torch.view_as_real(z / N - d).double())
     den = torch.linalg.vector_norm(torch.view_as_real(d).double())
     assert (num / den).item() <= 2 * oracle.tolerance(N)
+
+
+def transposed_pos(N, P, k):
+    """Position of X[k] in the FFTC_DIST_TRANSPOSED_OUT layout:
+    out[p*N/P + k1*Mp + jl] = X[p*Mp + jl + M*k1]."""
+    M, K, _, _ = fftc.fftc_dist_split(N, P)
+    Mp = M // P
+    k = np.asarray(k, dtype=np.int64)
+    j, k1 = k % M, k // M
+    return (j // Mp) * (N // P) + k1 * Mp + j % Mp
+
+
+@pytest.mark.parametrize("N,P", [(1 << 16, 2), (1 << 20, 4), (1 << 20, 8), (1 << 26, 4)])
+@pytest.mark.parametrize("flags", [fftc.FFTC_DIST_PEER_STORES, fftc.FFTC_DIST_TRANSPOSED_OUT,
+                                   fftc.FFTC_DIST_PEER_STORES | fftc.FFTC_DIST_TRANSPOSED_OUT])
+@pytest.mark.parametrize("sign", [-1, 1])
+def test_six_step_fused_exchange_and_transposed_output(N, P, flags, sign):
+    """NEXT-1 in loopback: the fused peer-store exchanges (the pack and DFT_M kernels store each
+    chunk straight into the receiving rank's buffer) and the transposed output (no
+    all-to-all #3), against the oracle; K > 4096 (two-pass DFT_K) at 2^26."""
+    x = synth.uniform_c64(N, 1, seed=N + P + flags)[0]
+    y, desc = run_dist(x, sign, P, flags=flags)
+    assert ("peer-stores" in desc) == bool(flags & fftc.FFTC_DIST_PEER_STORES), desc
+    yh = y.cpu().numpy()
+    if flags & fftc.FFTC_DIST_TRANSPOSED_OUT:
+        assert "output=transposed" in desc and "a2a=2" in desc
+        yh = yh[transposed_pos(N, P, np.arange(N))]  # back to natural order
+    if N <= (1 << 22):
+        ref = oracle.fft_ct(x[None], sign)[0]
+        err = oracle.rel_l2(yh[None], ref[None]).max()
+        assert err <= min(oracle.tolerance(N), 2e-6), (N, P, flags, err)
+    else:
+        _spot_and_parseval(x, yh, sign, nbins=8)

@@ -78,9 +78,10 @@ def main():
     N = 1 << 30
     x = torch.randn(N, dtype=torch.complex64, device=dev)
     y = torch.empty_like(x)
-    for P in (1, 8):
-        p = fftc.Plan.dist(N, -1, None, 0, P, loopback=P > 1)
-        row("six_step_loopback_P%d" % P, N, 1, p, timed(p, x, y, 3))
+    for P, flags in ((1, 0), (8, 0), (8, fftc.FFTC_DIST_PEER_STORES),
+                     (8, fftc.FFTC_DIST_PEER_STORES | fftc.FFTC_DIST_TRANSPOSED_OUT)):
+        p = fftc.Plan.dist(N, -1, None, 0, P, loopback=P > 1, flags=flags)
+        row("six_step_loopback_P%d_flags%d" % (P, flags), N, 1, p, timed(p, x, y, 3))
         p.close()
 
 
