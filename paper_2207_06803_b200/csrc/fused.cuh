@@ -30,6 +30,11 @@ namespace fftc {
 
 enum Map : int { LT_FAST = 0, F_FAST = 1 };
 
+#ifndef FFTC_TW_LOAD_ALL
+#define FFTC_TW_LOAD_ALL 0  // measured on B200: loading every twiddle is slower (L1-bound): 3125 199 -> 216 us
+#endif
+constexpr bool kTwLoadAll = FFTC_TW_LOAD_ALL != 0;
+
 constexpr int highbit(int r) {
   int h = 1;
   while (h * 2 <= r) h *= 2;
@@ -154,14 +159,17 @@ __device__ __forceinline__ void stage(float2* sm, int f, int lt, bool fvalid,
     if (fvalid && (EXACT || j < NB)) {
       const int m = (Ns == 1) ? 0 : (j % Ns);
       if constexpr (s > 0) {
-        // w_L^{m r}: table loads for r = 1, 2, 4, 8, ...; every other r as the product
-        // w^{2^b} w^{r - 2^b} (at most log2(R)-1 roundings deep)
+        // w_L^{m r}: power-of-two radices load r = 1, 2, 4, 8, ... from the table and form
+        // every other r as the product w^{2^b} w^{r - 2^b} (at most log2(R)-1 roundings deep);
+        // other radices load every r (the table holds them all): one load instead of a
+        // 4-instruction complex product, for the issue-bound odd-radix sizes
+        constexpr bool LOAD_ALL = kTwLoadAll && (R & (R - 1)) != 0;
         const float2* t = tw + (Ns - 1) + m;
         float2 w[R];
         sfor<R - 1>([&](auto r_) {
           constexpr int r = decltype(r_)::value + 1;
           constexpr int hb = highbit(r);
-          if constexpr (hb == r) w[r] = __ldg(t + (r - 1) * Ns);
+          if constexpr (LOAD_ALL || hb == r) w[r] = __ldg(t + (r - 1) * Ns);
           else w[r] = cmul(w[hb], w[r - hb]);
           v[k][r] = cmul(v[k][r], w[r]);
         });

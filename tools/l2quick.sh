@@ -1,3 +1,5 @@
 cd $GRAFT_REPO_ROOT
-timeout 900 python -m pytest tests/test_gpu_dist.py -v -m gpu -p no:cacheprovider --timeout 300 -x > gpurun_out/dist.log 2>&1
-grep -E "^E|FAILED|passed|failed" gpurun_out/dist.log | head -20
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -m gpu -p no:cacheprovider --timeout 300 -x -k "config3 or small_batches or candidate" 2>&1 | tail -1
+python bench.py --workload c3 --no-e2e --no-cpu --steps 10 | python -c "
+import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(d['value'], d['roofline']['frac'])
+for j in d['per_job']: print(j['N'], j['us'], j['eff_GBs'])"
