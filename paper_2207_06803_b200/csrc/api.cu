@@ -376,11 +376,16 @@ fftc_status fftc_execute_host(fftc_plan* p, const void* host_in, void* host_out)
     HostStage* hs = new HostStage();
     p->hs = hs;
     // ~32 MiB per chunk, at least one transform
-    int64_t chunk = ((int64_t)32 << 20) / tbytes;
+    int64_t chunk_bytes = (int64_t)32 << 20;  // tuning: FFTC_HOST_CHUNK_MB, FFTC_HOST_DEPTH
+    if (const char* c = getenv("FFTC_HOST_CHUNK_MB")) chunk_bytes = atoll(c) << 20;
+    if (const char* dpt = getenv("FFTC_HOST_DEPTH")) hs->depth = atoi(dpt);
+    if (hs->depth < 2) hs->depth = 2;
+    if (hs->depth > HostStage::kDepth) hs->depth = HostStage::kDepth;
+    int64_t chunk = chunk_bytes / tbytes;
     if (chunk < 1) chunk = 1;
     if (chunk > p->batch) chunk = p->batch;
     hs->chunk = chunk;
-    for (int i = 0; i < HostStage::kDepth && e == cudaSuccess; ++i) {
+    for (int i = 0; i < hs->depth && e == cudaSuccess; ++i) {
       e = cudaMalloc(&hs->d_in[i], (size_t)(chunk * tbytes));
       if (e == cudaSuccess) e = cudaMalloc(&hs->d_out[i], (size_t)(chunk * tbytes));
       if (e == cudaSuccess && (p->kind == KIND_FOURSTEP || p->kind == KIND_PASSES || p->kind == KIND_GPASS))
@@ -394,7 +399,7 @@ fftc_status fftc_execute_host(fftc_plan* p, const void* host_in, void* host_out)
   const char* hin = (const char*)host_in;
   char* hout = (char*)host_out;
   int k = 0;
-  for (int64_t t0 = 0; t0 < p->batch && e == cudaSuccess; t0 += hs->chunk, k = (k + 1) % HostStage::kDepth) {
+  for (int64_t t0 = 0; t0 < p->batch && e == cudaSuccess; t0 += hs->chunk, k = (k + 1) % hs->depth) {
     const int64_t nb = (p->batch - t0 < hs->chunk) ? p->batch - t0 : hs->chunk;
     const size_t bytes = (size_t)(nb * tbytes);
     e = cudaMemcpyAsync(hs->d_in[k], hin + t0 * tbytes, bytes, cudaMemcpyHostToDevice, hs->st[k]);
@@ -402,7 +407,7 @@ fftc_status fftc_execute_host(fftc_plan* p, const void* host_in, void* host_out)
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(hout + t0 * tbytes, hs->d_out[k], bytes, cudaMemcpyDeviceToHost, hs->st[k]);
   }
-  for (int i = 0; i < HostStage::kDepth; ++i) {
+  for (int i = 0; i < hs->depth; ++i) {
     cudaError_t s = cudaStreamSynchronize(hs->st[i]);
     if (e == cudaSuccess) e = s;
   }

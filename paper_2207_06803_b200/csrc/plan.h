@@ -18,7 +18,8 @@ enum PlanKind : int { KIND_COPY = 0, KIND_FUSED = 1, KIND_GENERIC = 2, KIND_FOUR
 struct DistState;  // dist.cu
 
 struct HostStage {  // fftc_execute_host pipeline buffers
-  static constexpr int kDepth = 3;
+  static constexpr int kDepth = 4;  // max streams / staging slots
+  int depth = 3;                     // used (FFTC_HOST_DEPTH)
   int64_t chunk = 0;  // transforms per chunk
   float2* d_in[kDepth] = {};
   float2* d_out[kDepth] = {};
