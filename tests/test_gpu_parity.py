@@ -112,6 +112,29 @@ def test_every_pass_candidate(n, name, monkeypatch):
         check(gpu_fft(x, sign), x, sign)
 
 
+# ---------------------------------------------------------------- every single-pass size
+def _smooth7(n):
+    for q in (2, 3, 5, 7):
+        while n % q == 0:
+            n //= q
+    return n == 1
+
+
+ALL_SMOOTH = [n for n in range(2, 4097) if _smooth7(n)]
+
+
+def test_every_7smooth_size_up_to_4096():
+    """Every 7-smooth N <= 4096 the planner accepts (247 sizes; compiled or runtime
+    schedule), batch 3, both signs, against the oracle."""
+    worst = 0.0
+    for N in ALL_SMOOTH:
+        x = synth.uniform_c64(N, 3, seed=N)
+        for sign in (-1, 1):
+            y = gpu_fft(x, sign)
+            worst = max(worst, check(y, x, sign))
+    assert worst <= 2e-6
+
+
 # ---------------------------------------------------------------- any 7-smooth N > 4096
 GPASS = [(12288, 9), (13122, 7), (15625, 5), (16807, 5), (19683, 5), (40960, 3), (46656, 3), (59049, 3),
          (78125, 2), (100000, 2), (248832, 2), (10 ** 6, 1), (3 ** 13, 1)]

@@ -12,6 +12,6 @@ python bench.py --workload c4 --steps 2 --warmup 3 --no-e2e --no-cpu > $OUT/plai
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 100 --csv --log-file $OUT/launches_c4.csv python bench.py --workload c4 --steps 2 --warmup 3 --no-e2e --no-cpu > $OUT/ncu_c4.log 2>&1
 python bench.py --workload c3 --steps 2 --warmup 3 --no-e2e --no-cpu > $OUT/plain3.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 100 --csv --log-file $OUT/launches_c3.csv python bench.py --workload c3 --steps 2 --warmup 3 --no-e2e --no-cpu > $OUT/ncu_c3.log 2>&1
-ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:\(int\)4096" -c 1 -o $OUT/prof_n4096 python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu > $OUT/ncu_full.log 2>&1
+ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:\\(int\\)4096" -c 1 -o $OUT/prof_n4096 python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu > $OUT/ncu_full.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_pass -c 2 -o $OUT/prof_pass python bench.py --workload c4 --steps 1 --warmup 1 --no-e2e --no-cpu > $OUT/ncu_full4.log 2>&1
 ls -la $OUT
