@@ -230,11 +230,15 @@ def run_fftc(args):
     # per-job numbers (rank-local, mean over steps)
     per_job = []
     for i, (N, b, s, d) in enumerate(jobs):
-        t = statistics.mean(launch_ms[k][i] for k in range(K)) / 1e3
+        ts = sorted(launch_ms[k][i] / 1e3 for k in range(K))
+        t = statistics.mean(ts)
         passes = plans[i].launches() if N > 4096 else 1  # HBM round trips (one per pass kernel)
         per_job.append({"N": N, "batch": b, "sign": s, "us": round(t * 1e6, 2),
+                        "us_median": round(ts[len(ts) // 2] * 1e6, 2), "us_min": round(ts[0] * 1e6, 2),
+                        "us_p90": round(ts[min(len(ts) - 1, int(0.9 * len(ts)))] * 1e6, 2),
                         "gflops": round(flops(N, b) / t / 1e9, 1),
-                        "eff_GBs": round(16 * N * b / t / 1e9, 1), "hbm_passes": passes})
+                        "eff_GBs": round(16 * N * b / t / 1e9, 1), "hbm_passes": passes,
+                        "plan": plans[i].describe()})
 
     # roofline of the dominant kernel family: the fused single-pass kernel (jobs with N <= 4096)
     # or, for large-N workloads, the TMA pass kernels (16 B per element per HBM pass)
