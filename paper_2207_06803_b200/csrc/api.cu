@@ -70,6 +70,13 @@ float2* upload_root_table(int64_t N, int64_t count, int64_t step, cudaError_t* e
   return d;
 }
 
+// split of a two-level root table for w_T^e, e < T: 2^sh low entries, T / 2^sh + 1 high ones
+int balanced_split(int64_t T) {
+  int n = 0;
+  while (((int64_t)1 << n) < T) ++n;
+  return (n + 1) / 2;
+}
+
 cudaError_t exec_local(const fftc_plan* p, const float2* in, float2* out, long long batch, float2* work,
                        cudaStream_t st) {
   const int conj = p->sign > 0;
@@ -282,8 +289,10 @@ fftc_plan* fftc_plan_create(int64_t N, int64_t batch, int sign) {
         if (!pe) return fail(p, FFTC_ERROR_UNSUPPORTED_SIZE);
         const int64_t T = Ns * Ls2[s];
         d.tw[s] = upload_stage_table(Ls2[s], pe->R, pe->S, &err);
-        if (err == cudaSuccess) d.twA[s] = upload_root_table(T, T < 4096 ? T : 4096, 1, &err);
-        if (err == cudaSuccess) d.twB[s] = upload_root_table(T, (T + 4095) / 4096, 4096, &err);
+        d.tws[s] = balanced_split(T);
+        if (err == cudaSuccess) d.twA[s] = upload_root_table(T, (int64_t)1 << d.tws[s], 1, &err);
+        if (err == cudaSuccess)
+          d.twB[s] = upload_root_table(T, (T >> d.tws[s]) + 1, (int64_t)1 << d.tws[s], &err);
         Ns = T;
       }
       if (err == cudaSuccess && batch > 0) err = cudaMalloc(&p->d_work, l2_work_bytes(d, batch));
@@ -312,8 +321,10 @@ fftc_plan* fftc_plan_create(int64_t N, int64_t batch, int sign) {
       p->pp.e[s] = e;
       const int64_t T = Ns * Ls[s];
       p->pp.tw[s] = upload_stage_table(Ls[s], e->R, e->S, &err);
-      if (err == cudaSuccess) p->pp.twA[s] = upload_root_table(T, T < 4096 ? T : 4096, 1, &err);
-      if (err == cudaSuccess) p->pp.twB[s] = upload_root_table(T, (T + 4095) / 4096, 4096, &err);
+      p->pp.tws[s] = balanced_split(T);
+      if (err == cudaSuccess) p->pp.twA[s] = upload_root_table(T, (int64_t)1 << p->pp.tws[s], 1, &err);
+      if (err == cudaSuccess)
+        p->pp.twB[s] = upload_root_table(T, (T >> p->pp.tws[s]) + 1, (int64_t)1 << p->pp.tws[s], &err);
       Ns = T;
     }
     if (err == cudaSuccess && batch > 0 && np > 1) err = cudaMalloc(&p->d_work, (size_t)(N * batch) * sizeof(float2));

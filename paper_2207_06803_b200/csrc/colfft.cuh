@@ -29,6 +29,12 @@ __device__ __forceinline__ float2 root_lookup(const float2* __restrict__ A, cons
                                               long long e) {
   return cmul(__ldg(A + (e & 4095)), __ldg(B + (e >> 12)));
 }
+// the same with a balanced split (A: 2^sh entries w_T^t, B: w_T^{2^sh h}): both tables stay
+// small enough to live in L1 next to the pass kernels' shared-memory tiles
+__device__ __forceinline__ float2 root_lookup_s(const float2* __restrict__ A, const float2* __restrict__ B,
+                                                long long e, int sh) {
+  return cmul(__ldg(A + (e & ((1LL << sh) - 1))), __ldg(B + (e >> sh)));
+}
 
 template <class P, bool OUT_T, int MINB>
 __global__ void __launch_bounds__(P::THREADS, MINB)

@@ -209,11 +209,11 @@ __global__ void __launch_bounds__(kThreads, MINB) k_l2(const __grid_constant__ L
     if (threadIdx.x == 0 && it.s > 0) red_release_gpu_add(rdone(q, it.c, it.s), 1u);  // input slot read
     const float ci = it.s == 0 ? q.csign : 1.f, co = it.s == q.p - 1 ? q.csign : 1.f;
     if (it.s == 0) {  // pass 0 always runs the long schedule (lengths are non-increasing)
-      pass_tile<CA, false>(sm, f, lt, c0 + f, 1, ps.tw, ps.twA, ps.twB, ci, co);
+      pass_tile<CA, false>(sm, f, lt, c0 + f, 1, ps.tw, ps.twA, ps.twB, ps.tws, ci, co);
     } else if (ps.which == 0) {
-      pass_tile<CA, true>(sm, f, lt, c0 + f, ps.Ns, ps.tw, ps.twA, ps.twB, ci, co);
+      pass_tile<CA, true>(sm, f, lt, c0 + f, ps.Ns, ps.tw, ps.twA, ps.twB, ps.tws, ci, co);
     } else {
-      pass_tile<CB, true>(sm, f, lt, c0 + f, ps.Ns, ps.tw, ps.twA, ps.twB, ci, co);
+      pass_tile<CB, true>(sm, f, lt, c0 + f, ps.Ns, ps.tw, ps.twA, ps.twB, ps.tws, ci, co);
     }
     if (threadIdx.x == 0) flush();  // the previous tile's stores had a whole tile of compute to land
     if (it.s == 0) {
@@ -425,6 +425,7 @@ cudaError_t l2_execute(const L2PlanData& d, const float2* in, float2* out, void*
     ps.tw = d.tw[s];
     ps.twA = d.twA[s];
     ps.twB = d.twB[s];
+    ps.tws = d.tws[s];
     bool ok = s == 0 ? map_cols(&q.ld[0], in, d.N, d.L[0], batch) : map_cols(&q.ld[s], q.ring, d.N, d.L[s], ring_b);
     if (ok && s > 0)
       ok = s == d.p - 1 ? map_autosort(&q.st[s], out, d.N, d.L[s], Ns, batch)

@@ -15,8 +15,9 @@ struct L2Stage {  // one pass of the plan
   int Ns;         // product of the earlier pass lengths
   int T;          // column tiles (of 16) per transform = N / L / 16
   const float2* tw;   // stage twiddles of DFT_L
-  const float2* twA;  // w_{Ns L}^t, t < 4096
-  const float2* twB;  // w_{Ns L}^{4096 h}
+  const float2* twA;  // w_{Ns L}^t, t < 2^tws
+  const float2* twB;  // w_{Ns L}^{2^tws h}
+  int tws;            // twiddle table split
 };
 
 // Kernel parameters (one __grid_constant__ struct; the tensor maps must stay 64-byte aligned).
@@ -50,6 +51,7 @@ struct L2PlanData {
   float2* tw[kMaxL2Passes] = {};
   float2* twA[kMaxL2Passes] = {};
   float2* twB[kMaxL2Passes] = {};
+  int tws[kMaxL2Passes] = {};
 };
 
 // Pass lengths of the L2 path: p = 2 for 2^13..2^16, p = 3 for 2^17..2^21, each in

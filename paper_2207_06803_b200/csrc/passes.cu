@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(P::THREADS, MINB)
     const int b = (int)(t / tpb), c0 = (int)(t % tpb) * C;
     const int c = c0 + f;
     mbar_wait(&full[k], NBUF == 2 ? ((it >> 1) & 1) : (it & 1));
-    pass_tile<P, !FIRST>(sm, f, lt, c, g.Ns, tw, twA, twB, csign_in, csign_out);
+    pass_tile<P, !FIRST>(sm, f, lt, c, g.Ns, tw, twA, twB, g.tws, csign_in, csign_out);
     if constexpr (!FIRST) {
       fence_proxy_async_smem();
       __syncthreads();
@@ -250,6 +250,7 @@ cudaError_t passes_execute(const PassPlanData& pp, const float2* in, float2* out
     g.Ns = (int)Ns;
     g.N = pp.N;
     g.tw = s > 0;
+    g.tws = pp.tws[s];
     cudaError_t err = e->launch(s == 0, tin, tout, dst, pp.tw[s], pp.twA[s], pp.twB[s], g, conj && s == 0,
                                 conj && s == p - 1, st);
     if (err != cudaSuccess) return err;

@@ -12,6 +12,7 @@ struct PassGeom {
   int Ns;                 // Stockham Ns of this pass (product of earlier pass lengths)
   long long N;
   int tw;                 // apply the input twiddle w_{Ns L}^{(c mod Ns) r}
+  int tws;                // twiddle table split: twA holds 2^tws entries
 };
 
 typedef cudaError_t (*pass_launch_fn)(bool first, const CUtensorMap& tin, const CUtensorMap& tout, float2* out_first,
@@ -34,8 +35,9 @@ struct PassPlanData {
   int p = 0;
   const PassEntry* e[kMaxPasses] = {};
   float2* tw[kMaxPasses] = {};   // stage twiddles of DFT_{L_s}
-  float2* twA[kMaxPasses] = {};  // w_{Ns L}^t, t < 4096
-  float2* twB[kMaxPasses] = {};  // w_{Ns L}^{4096 h}
+  float2* twA[kMaxPasses] = {};  // w_{Ns L}^t, t < 2^tws
+  float2* twB[kMaxPasses] = {};  // w_{Ns L}^{2^tws h}
+  int tws[kMaxPasses] = {};      // split of the pass twiddle tables (balanced: ceil(log2(Ns L) / 2))
 };
 
 const PassEntry* find_pass(int L);

@@ -17,11 +17,13 @@
 namespace fftc {
 
 // DFT_L of the C columns of the tile, in place.  c = this thread's column (c0 + f);
-// the input twiddle w_{Ns L}^{(c mod Ns) i} is applied when TW (every pass but the first).
+// the input twiddle w_{Ns L}^{(c mod Ns) i} is applied when TW (every pass but the first), read
+// as twA[e mod 2^tws] * twB[e >> tws] (tables built in double on the host).
 template <class P, bool TW>
 __device__ __forceinline__ void pass_tile(float2* sm, int f, int lt, int c, int Ns,
                                           const float2* __restrict__ tw, const float2* __restrict__ twA,
-                                          const float2* __restrict__ twB, float csign_in, float csign_out) {
+                                          const float2* __restrict__ twB, int tws, float csign_in,
+                                          float csign_out) {
   static_assert((P::FPB == 16 && P::LAY == LAY_TMA128) || (P::FPB == 8 && P::LAY == LAY_TMA64),
                 "pass tiles: 16 columns with the TMA 128B swizzle or 8 columns with the 64B swizzle");
   constexpr int L = P::N;
@@ -32,7 +34,7 @@ __device__ __forceinline__ void pass_tile(float2* sm, int f, int lt, int c, int 
   const long long m = TW ? (long long)(c % Ns) : 0;
   float2 sp[NB2];
   if constexpr (TW) {
-    sp[0] = root_lookup(twA, twB, m * NB0);
+    sp[0] = root_lookup_s(twA, twB, m * NB0, tws);
     sfor<NB2 - 1>([&](auto b_) {
       constexpr int bb = decltype(b_)::value + 1;
       sp[bb] = cmul(sp[bb - 1], sp[bb - 1]);
@@ -43,7 +45,7 @@ __device__ __forceinline__ void pass_tile(float2* sm, int f, int lt, int c, int 
     float2 v = sm[P::sidx(f, i)];
     v.y *= csign_in;
     if constexpr (TW) {
-      if (r == 0) base = root_lookup(twA, twB, m * i);
+      if (r == 0) base = root_lookup_s(twA, twB, m * i, tws);
       float2 w = base;
       sfor<NB2>([&](auto b_) {
         constexpr int bb = decltype(b_)::value;

@@ -1,13 +1,5 @@
 cd $GRAFT_REPO_ROOT
-for cfg in "32 3" "8 3" "16 4" "64 3" "128 2" "16 3"; do set -- $cfg; FFTC_HOST_CHUNK_MB=$1 FFTC_HOST_DEPTH=$2 python - <<'PY'
-import sys, os, time, torch; sys.path.insert(0,'.')
-import paper_2207_06803_b200 as fftc
-N=1024; b=(1<<26)//N
-x=torch.randn(N*b,dtype=torch.complex64).pin_memory(); y=torch.empty_like(x).pin_memory()
-p=fftc.Plan(N,b,-1); p.execute_host(x,y)
-t=time.perf_counter()
-for _ in range(5): p.execute_host(x,y)
-t=(time.perf_counter()-t)/5
-print(os.environ['FFTC_HOST_CHUNK_MB'], os.environ['FFTC_HOST_DEPTH'], 'ms', round(t*1e3,2), 'GB/s per direction', round(8*N*b/t/1e9,1))
-PY
-done
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -m gpu -p no:cacheprovider --timeout 300 -x -k "multipass or l2 or fourstep_small or pass_candidate or config4" 2>&1 | tail -1
+python bench.py --workload c4 --no-e2e --no-cpu --steps 10 | python -c "
+import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(d['value'], d['roofline']['frac'])
+for j in d['per_job']: print(j['N'], j['sign'], j['us'], j['eff_GBs'])"
