@@ -144,10 +144,18 @@ static const PassEntry kPasses[] = {
     FFTC_PASS("p16_r4x4", 16, PRad_4x4, 4, 8, 2, 4, 4),
     FFTC_PASS("p32_r8x4", 32, PRad_8x4, 4, 8, 2, 8, 4),
     FFTC_PASS("p64_r8x8", 64, PRad_8x8, 8, 6, 2, 8, 8),
+    FFTC_PASS("p64_r8x8_m4", 64, PRad_8x8, 8, 4, 2, 8, 8),
     FFTC_PASS("p128_r16x8", 128, PRad_16x8, 16, 3, 2, 16, 8),
+    FFTC_PASS("p128_r16x8_b2m2", 128, PRad_16x8, 16, 2, 2, 16, 8),
+    FFTC_PASS("p128_r16x8_b2m4", 128, PRad_16x8, 16, 4, 2, 16, 8),
+    FFTC_PASS("p256_r16x16_b2m2", 256, PRad_16x16, 16, 2, 2, 16, 16),
     FFTC_PASS("p256_r16x16", 256, PRad_16x16, 16, 3, 2, 16, 16),
+    FFTC_PASS("p256_r16x16_b2m1", 256, PRad_16x16, 16, 1, 2, 16, 16),
+    FFTC_PASS("p256_r16x16_b1m4", 256, PRad_16x16, 16, 4, 1, 16, 16),
     FFTC_PASS8("p512_r16x32_c8t32", 512, PRad_16x32, 32, 2, 2, 16, 32),
     FFTC_PASS8("p512_r32x16_c8", 512, PRad_32x16, 16, 3, 2, 32, 16),
+    FFTC_PASS8("p512_r32x16_c8m2", 512, PRad_32x16, 16, 2, 2, 32, 16),
+    FFTC_PASS8("p512_r16x32_c8t32m1", 512, PRad_16x32, 32, 1, 2, 16, 32),
     FFTC_PASS8("p1024_r32x32_c8b2", 1024, PRad_32x32, 32, 1, 2, 32, 32),
     FFTC_PASS8("p1024_r32x32_c8b1", 1024, PRad_32x32, 32, 3, 1, 32, 32),
 };

@@ -1,5 +1,5 @@
 cd $GRAFT_REPO_ROOT
-timeout 900 python -m pytest tests/test_gpu_parity.py -q -m gpu -p no:cacheprovider --timeout 300 -x -k "multipass or l2 or fourstep_small or pass_candidate or config4" 2>&1 | tail -1
-python bench.py --workload c4 --no-e2e --no-cpu --steps 10 | python -c "
-import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(d['value'], d['roofline']['frac'])
-for j in d['per_job']: print(j['N'], j['sign'], j['us'], j['eff_GBs'])"
+for k in p256_r16x16_b2m2 p256_r16x16_b2m1; do for n in 16 24; do FFTC_PASS=$k timeout 100 python tools/l2sweep.py one $n $(( (1<<28) >> n )) | cut -c1-110; done; done
+for k in p128_r16x8 p128_r16x8_b2m2; do for n in 14 21; do FFTC_PASS=$k timeout 100 python tools/l2sweep.py one $n $(( (1<<28) >> n )) | cut -c1-110; done; done
+for k in p512_r16x32_c8t32 p512_r32x16_c8m2 p512_r16x32_c8t32m1; do FFTC_PASS=$k timeout 100 python tools/l2sweep.py one 18 1024 | cut -c1-110; done
+for k in p64_r8x8 p64_r8x8_m4; do FFTC_PASS=$k timeout 100 python tools/l2sweep.py one 13 32768 | cut -c1-110; done
