@@ -19,7 +19,16 @@ namespace fftc {
 // DFT_L of the C columns of the tile, in place.  c = this thread's column (c0 + f);
 // the input twiddle w_{Ns L}^{(c mod Ns) i} is applied when TW (every pass but the first), read
 // as twA[e mod 2^tws] * twB[e >> tws] (tables built in double on the host).
-template <class P, bool TW>
+// Shared-memory position of output k of column f for the first pass's TMA store: rows of 16
+// consecutive outputs (128 B), row (k / 16) * C + f, 16-byte chunks XOR-swizzled by (f & 7) --
+// the 128B-swizzled box [16 k][C columns][L / 16] of the (k % 16, c, k / 16, batch) view of a
+// pass-0 output, where column c's L outputs are contiguous.
+template <class P>
+__device__ __forceinline__ int out0_idx(int f, int k) {
+  return (((k >> 4) * P::FPB + f) << 4) + ((((k & 15) >> 1) ^ (f & 7)) << 1) + (k & 1);
+}
+
+template <class P, bool TW, bool OUT0 = false>
 __device__ __forceinline__ void pass_tile(float2* sm, int f, int lt, int c, int Ns,
                                           const float2* __restrict__ tw, const float2* __restrict__ twA,
                                           const float2* __restrict__ twB, int tws, float csign_in,
@@ -55,7 +64,11 @@ __device__ __forceinline__ void pass_tile(float2* sm, int f, int lt, int c, int 
     }
     return v;
   };
-  auto gstore = [&](int i, float2 v, int) { sm[P::sidx(f, i)] = make_float2(v.x, csign_out * v.y); };
+  // the last sub-stage writes in place (all reads precede it); OUT0: in the pass-0 store layout
+  auto gstore = [&](int i, float2 v, int) {
+    if constexpr (OUT0) sm[out0_idx<P>(f, i)] = make_float2(v.x, csign_out * v.y);
+    else sm[P::sidx(f, i)] = make_float2(v.x, csign_out * v.y);
+  };
   // sub-stages of DFT_L in place on the tile (every stage reads all, syncs, writes)
   sfor<P::S>([&](auto s_) {
     constexpr int s = decltype(s_)::value;
