@@ -236,8 +236,9 @@ static bool map_out(CUtensorMap* m, void* base, long long N, int L, int C, long 
 bool passes_available() { return get_encode() != nullptr; }
 
 // Split N (power of two, 2^9 .. 2^48) into p passes: p = ceil(log2 N / 8) with lengths in
-// [16, 256], except that 2^17 .. 2^20 take two passes of up to 1024 (8-column tiles) --
-// one HBM round trip fewer (env FFTC_PASS_MAXLOG=8 restores three passes).  Lengths are
+// [16, 256], except that 2^17 .. 2^20 take two passes of up to 1024 and 2^25 .. 2^28 three
+// passes [<= 1024, <= 1024, 256] -- one HBM round trip fewer (measured on B200, profiles/r01h;
+// env FFTC_PASS_MAXLOG=8 restores the short passes).  Lengths are
 // as equal as possible, larger first.
 int pass_split(long long N, int* Ls, int max) {
   if (N < 512 || (N & (N - 1))) return -1;
@@ -247,8 +248,30 @@ int pass_split(long long N, int* Ls, int max) {
   if (const char* m = getenv("FFTC_PASS_MAXLOG")) maxlog = atoi(m);
   if (maxlog < 8) maxlog = 8;
   if (maxlog > 10) maxlog = 10;
+  if (const char* fl = getenv("FFTC_PASS_LOGS")) {  // tuning: explicit log2 lengths, e.g. "10,9,8"
+    int q = 0, sum = 0;
+    for (const char* c = fl; *c && q < max;) {
+      const int e = atoi(c);
+      if (e < 4 || e > 10) return -1;
+      Ls[q++] = 1 << e;
+      sum += e;
+      while (*c && *c != ',') ++c;
+      if (*c == ',') ++c;
+    }
+    if (sum == n) return q;
+  }
   int p = (n + 7) / 8;
-  if (p == 3 && n <= 2 * maxlog) p = 2;
+  if (p == 3 && n <= 2 * maxlog) p = 2;  // 2^17 .. 2^20: two passes of <= 1024
+  if (p == 4 && n <= 2 * maxlog + 8) {
+    // 2^25 .. 2^28: three passes, the last one 256 long (16-column tiles: its autosort store
+    // writes 128-byte rows; 8-column tiles there scatter 64-byte rows at MB strides, slower)
+    if (max < 3) return -1;
+    const int m = n - 8;
+    Ls[0] = 1 << ((m + 1) / 2);
+    Ls[1] = 1 << (m / 2);
+    Ls[2] = 256;
+    return 3;
+  }
   if (p > max) return -1;
   for (int s = 0; s < p; ++s) {
     const int e = n / p + (s < n % p ? 1 : 0);

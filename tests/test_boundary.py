@@ -90,10 +90,16 @@ def test_planner_passes():
     for n in range(9, 41):
         Ls = fftc.fftc_plan_passes(1 << n)
         assert Ls is not None and math.prod(Ls) == 1 << n
-        want = 2 if 17 <= n <= 20 else (n + 7) // 8  # 2^17..2^20: two passes of <= 1024
+        # 2^17..2^20: two passes of <= 1024, 2^25..2^28: three (last 256); else ceil(n/8) of <= 256
+        big = 17 <= n <= 20 or 25 <= n <= 28
+        want = 2 if 17 <= n <= 20 else 3 if 25 <= n <= 28 else (n + 7) // 8
+        if 25 <= n <= 28:
+            assert Ls[-1] == 256
         assert len(Ls) == want, (n, Ls)
-        assert all(16 <= L <= (1024 if want == 2 else 256) for L in Ls)
-        assert Ls == sorted(Ls, reverse=True) and max(Ls) <= 2 * min(Ls)
+        assert all(16 <= L <= (1024 if big else 256) for L in Ls)
+        assert Ls == sorted(Ls, reverse=True)
+        if not 25 <= n <= 28:
+            assert max(Ls) <= 2 * min(Ls)  # balanced
     assert fftc.fftc_plan_passes(3 * 4096) is None
     assert fftc.fftc_plan_passes(256) is None
 

@@ -211,6 +211,33 @@ def test_l2_matches_hbm_multipass(n, monkeypatch):
     assert d.max() <= 2e-7, float(d.max())
 
 
+@pytest.mark.parametrize("n", [25, 26, 27, 28])
+def test_multipass_three_long_passes(n):
+    """2^25..2^28: three passes, 512/1024-long (8-column) tiles then a 256-long (16-column)
+    last pass.  Spot bins by direct summation (the definition), Parseval, and the round trip."""
+    N = 1 << n
+    x = synth.uniform_c64(N, 1, seed=n)
+    with fftc.Plan(N, 1, -1) as p:
+        assert "kind=passes" in p.describe() and p.launches() == 3, p.describe()
+    d = torch.from_numpy(x).cuda()
+    with fftc.Plan(N, 1, -1) as pf, fftc.Plan(N, 1, 1) as pi:
+        y = pf(d)
+        z = pi(y)
+    torch.cuda.synchronize()
+    yh = y.cpu().numpy()[0]
+    rng = np.random.default_rng(n)
+    scale = np.sqrt(N) * np.sqrt(np.mean(np.abs(x.astype(np.complex128)) ** 2))
+    for k in [0, 1, N // 2, N - 1] + rng.integers(0, N, 6).tolist():
+        ref = oracle.spot_bin(x, int(k), -1)
+        assert abs(yh[k] - ref) / scale <= 2e-6, (n, k)
+    ex = np.sum(np.abs(x.astype(np.complex128)) ** 2)
+    ey = np.sum(np.abs(yh.astype(np.complex128)) ** 2)
+    assert abs(ey / (N * ex) - 1) < 1e-5
+    rt = z.cpu().numpy()[0].astype(np.complex128) / N
+    err = np.sqrt(np.sum(np.abs(rt - x[0]) ** 2) / ex)
+    assert err <= 2 * oracle.tolerance(N), err
+
+
 @pytest.mark.parametrize("N", POW2 + MIXED)
 def test_every_candidate_schedule(N, monkeypatch):
     """Every compiled schedule (not just the planner's default) is correct, both signs, ragged batch."""
