@@ -112,6 +112,25 @@ def test_every_pass_candidate(n, name, monkeypatch):
         check(gpu_fft(x, sign), x, sign)
 
 
+# ---------------------------------------------------------------- beyond 2^31 elements
+@pytest.mark.parametrize("N,batch", [(64, (1 << 25) + 3), (4096, (1 << 19) + 5), (1 << 16, (1 << 15) + 1)])
+def test_more_than_2p31_elements(N, batch):
+    """batch*N > 2^31 (16 GiB buffers): 64-bit offsets in every kernel / tensor map.  Input
+    drawn on the device from a seeded generator; the oracle checks transforms sampled across
+    the whole batch, the last ones included."""
+    g = torch.Generator(device="cuda").manual_seed(N)
+    d = (torch.rand(batch * N * 2, device="cuda", generator=g, dtype=torch.float32) * 2 - 1).view(torch.complex64)
+    with fftc.Plan(N, batch, -1) as p:
+        y = p(d)
+    torch.cuda.synchronize()
+    idx = np.array([0, 1, batch // 3, batch // 2, (1 << 31) // N - 1, (1 << 31) // N, batch - 2, batch - 1])
+    xs = d.view(batch, N)[torch.from_numpy(idx).cuda()].cpu().numpy()
+    ys = y.view(batch, N)[torch.from_numpy(idx).cuda()].cpu().numpy()
+    del d, y
+    torch.cuda.empty_cache()
+    check(ys, xs, -1)
+
+
 # ---------------------------------------------------------------- every single-pass size
 def _smooth7(n):
     for q in (2, 3, 5, 7):
