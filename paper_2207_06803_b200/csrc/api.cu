@@ -175,13 +175,14 @@ static fftc_status setup_gpass(fftc_plan* p, const int* Lg, int pg, const int (*
     float2* t0 = upload_stage_table(Lg[s], g.R, g.S, &err);
     p->gp_tables[3 * s] = t0;
     g.tw = t0;
+    g.tws = balanced_split(T);
     if (err == cudaSuccess) {
-      float2* t1 = upload_root_table(T, T < 4096 ? T : 4096, 1, &err);
+      float2* t1 = upload_root_table(T, (int64_t)1 << g.tws, 1, &err);
       p->gp_tables[3 * s + 1] = t1;
       g.twA = t1;
     }
     if (err == cudaSuccess) {
-      float2* t2 = upload_root_table(T, (T + 4095) / 4096, 4096, &err);
+      float2* t2 = upload_root_table(T, (T >> g.tws) + 1, (int64_t)1 << g.tws, &err);
       p->gp_tables[3 * s + 2] = t2;
       g.twB = t2;
     }

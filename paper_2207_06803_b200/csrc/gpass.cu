@@ -53,15 +53,29 @@ __global__ void __launch_bounds__(kGpThreads, 4)
     s_cm[f] = c - (c / g.Ns) * g.Ns;
   }
   __syncthreads();
-  // stage in: lanes walk columns; input twiddle w_T^{(c mod Ns) r}, T = Ns L
+  // stage in: lanes walk columns; input twiddle w_T^{(c mod Ns) r}, T = Ns L.  Eight
+  // elements per thread per round: all loads first (memory-level parallelism), then the
+  // twiddles and the shared-memory stores.
   const float2* gi = in + b * N + c0;
-  for (int e = threadIdx.x; e < (L << lc); e += kGpThreads) {
-    const int f = e & (cols - 1), r = e >> lc;
-    if (f < nc) {
-      float2 v = __ldcs(gi + f + (long long)r * NB);
-      v.y *= csign_in;
-      if (g.Ns > 1) v = cmul(v, root_lookup(g.twA, g.twB, (long long)s_cm[f] * r));
-      A[f * LP + r] = v;
+  constexpr int U = 8;
+  for (int e0 = threadIdx.x; e0 < (L << lc); e0 += U * kGpThreads) {
+    float2 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * kGpThreads;
+      const int f = e & (cols - 1), r = e >> lc;
+      v[u] = (e < (L << lc) && f < nc) ? __ldcs(gi + f + (long long)r * NB) : make_float2(0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * kGpThreads;
+      const int f = e & (cols - 1), r = e >> lc;
+      if (e < (L << lc) && f < nc) {
+        float2 x = v[u];
+        x.y *= csign_in;
+        if (g.Ns > 1) x = cmul(x, root_lookup_s(g.twA, g.twB, (long long)s_cm[f] * r, g.tws));
+        A[f * LP + r] = x;
+      }
     }
   }
   __syncthreads();

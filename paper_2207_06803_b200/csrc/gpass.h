@@ -14,8 +14,9 @@ struct GPassStage {       // one pass (kernel argument)
   int S;                  // sub-stages of DFT_L
   int R[kMaxStages];      // their radices (generic codelet set)
   const float2* tw;       // stage twiddles of DFT_L
-  const float2* twA;      // w_{Ns L}^t, t < 4096
-  const float2* twB;      // w_{Ns L}^{4096 h}
+  const float2* twA;      // w_{Ns L}^t, t < 2^tws
+  const float2* twB;      // w_{Ns L}^{2^tws h}
+  int tws;                // balanced table split (both tables L1-resident)
 };
 
 struct GPassPlanData {
