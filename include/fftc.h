@@ -158,7 +158,8 @@ fftc_plan* fftc_plan_create_expr(const char* expr, int64_t batch, int sign);
 
 /* ---------------------------------------------------------------------
  * JIT mode: an N <= 4096 with prime factors above 7 (up to 61)
- * gets a single-pass kernel generated for that N -- Stockham stages, each
+ * gets a single-pass kernel generated for that N (larger such N: runtime
+ * passes, each a kernel generated for its length) -- Stockham stages, each
  * DFT_R a straight-line codelet emitted by Eq. 2 (primes: conjugate-pair
  * form of the definition) -- compiled by NVRTC for sm_100a when the plan
  * is created (fftc_plan_create; cached per N for the process).  Without
@@ -173,6 +174,11 @@ int fftc_jit_source(int64_t N, char* buf, size_t len);
  * sm_100a.  Returns the cubin size (> 0), or < 0 (-1 no NVRTC / not a JIT
  * size, -4 compile error); the NVRTC log goes to log (may be NULL).        */
 int fftc_jit_compile(int64_t N, char* log, size_t loglen);
+
+/* Host only: compile the JIT pass kernel for pass length L (<= 256, prime factors <= 61;
+ * the runtime multi-pass path above 4096 specialises each pass this way).  Returns the
+ * cubin size, or < 0 as fftc_jit_compile.                                 */
+int fftc_jit_pass_compile(int L, char* log, size_t loglen);
 
 /* The paper's "direct" DFT: y = DFT_N x as one dense
  * product per transform, batched into a GEMM on the tcgen05 tensor cores

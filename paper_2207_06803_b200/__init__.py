@@ -74,6 +74,7 @@ def load(path: str = LIB_PATH):
         "fftc_jit_source": ([i64, ctypes.c_char_p, sz], i32),
         "fftc_plan_create_direct": ([i64, i64, i32], vp),
         "fftc_jit_compile": ([i64, ctypes.c_char_p, sz], i32),
+        "fftc_jit_pass_compile": ([i32, ctypes.c_char_p, sz], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -176,6 +177,12 @@ def fftc_jit_compile(N: int):
     """NVRTC-compile the JIT kernel for N (host only) -> (cubin bytes or error code, log)."""
     log = ctypes.create_string_buffer(1 << 16)
     r = load().fftc_jit_compile(N, log, 1 << 16)
+    return r, log.value.decode(errors="replace")
+
+
+def fftc_jit_pass_compile(L: int):
+    log = ctypes.create_string_buffer(1 << 16)
+    r = load().fftc_jit_pass_compile(L, log, 1 << 16)
     return r, log.value.decode(errors="replace")
 
 

@@ -151,9 +151,13 @@ static void free_plan(fftc_plan* p) {
 
 static void free_plan(fftc_plan* p);
 
-// Runtime-schedule passes (gpass.cu) with explicit lengths and per-pass radices.
+// Runtime-schedule passes (gpass.cu) with explicit lengths and per-pass radices.  Each pass
+// gets an NVRTC kernel specialised to (L, radices) when NVRTC is there (FFTC_GPASS_JIT=0
+// keeps the compiled runtime-schedule kernel); radices outside the compiled codelet set need it.
 static fftc_status setup_gpass(fftc_plan* p, const int* Lg, int pg, const int (*R)[kMaxStages], const int* S) {
   cudaError_t err = cudaSuccess;
+  const char* ej = getenv("FFTC_GPASS_JIT");
+  const bool try_jit = jit_available() && !(ej && strcmp(ej, "0") == 0);
   p->kind = KIND_GPASS;
   p->gp.N = p->N;
   p->gp.p = pg;
@@ -163,14 +167,21 @@ static fftc_status setup_gpass(fftc_plan* p, const int* Lg, int pg, const int (*
     g.L = Lg[s];
     g.Ns = (int)Ns;
     g.S = S[s];
+    g.jk = nullptr;
     if (g.L > kGpassMaxL || g.S < 1 || g.S > kMaxStages) return FFTC_ERROR_UNSUPPORTED_SIZE;
     int64_t prod = 1;
+    bool generic = true;
     for (int t = 0; t < g.S; ++t) {
-      if (!generic_supports_radix(R[s][t])) return FFTC_ERROR_UNSUPPORTED_SIZE;
+      generic = generic && generic_supports_radix(R[s][t]);
       g.R[t] = R[s][t];
       prod *= R[s][t];
     }
     if (prod != g.L) return FFTC_ERROR_INVALID_VALUE;
+    if (try_jit) {
+      cudaError_t je = cudaSuccess;
+      g.jk = jit_pass_get(g.L, g.R, g.S, &je);
+    }
+    if (!g.jk && !generic) return FFTC_ERROR_UNSUPPORTED_SIZE;
     const int64_t T = Ns * Lg[s];
     float2* t0 = upload_stage_table(Lg[s], g.R, g.S, &err);
     p->gp_tables[3 * s] = t0;
@@ -218,7 +229,9 @@ fftc_plan* fftc_plan_create(int64_t N, int64_t batch, int sign) {
   if (N < 1 || batch < 0 || (sign != -1 && sign != 1)) return fail(nullptr, FFTC_ERROR_INVALID_VALUE);
   int Rj[32];
   const int Sj = seven_smooth(N) ? -1 : (N <= kGenericMaxN ? jit_radices((int)N, Rj, 32) : -1);
-  if (!seven_smooth(N) && Sj < 0) return fail(nullptr, FFTC_ERROR_UNSUPPORTED_SIZE);
+  int Lj[kMaxGPasses];
+  const int pj = (!seven_smooth(N) && N > kGenericMaxN) ? gpass_split(N, Lj, kMaxGPasses, kJitMaxPrime) : -1;
+  if (!seven_smooth(N) && Sj < 0 && pj < 0) return fail(nullptr, FFTC_ERROR_UNSUPPORTED_SIZE);
   if (batch > 0 && batch > ((int64_t)1 << 60) / (N * 8)) return fail(nullptr, FFTC_ERROR_UNSUPPORTED_SIZE);
   int dev = 0;
   fftc_status ds = fftc_check_device(&dev);
@@ -229,6 +242,19 @@ fftc_plan* fftc_plan_create(int64_t N, int64_t batch, int sign) {
   p->sign = sign;
   p->device = dev;
   cudaError_t err = cudaSuccess;
+  if (pj > 0) {
+    // above 4096 with prime factors 11..61: runtime passes, each an NVRTC-specialised kernel
+    if (!jit_available()) return fail(p, FFTC_ERROR_UNSUPPORTED_SIZE);
+    int R[kMaxGPasses][kMaxStages], S[kMaxGPasses];
+    for (int s = 0; s < pj; ++s) {
+      int tmp[32];
+      S[s] = jit_pass_radices(Lj[s], tmp, 32);
+      if (S[s] < 1 || S[s] > kMaxStages) return fail(p, FFTC_ERROR_UNSUPPORTED_SIZE);
+      for (int t = 0; t < S[s]; ++t) R[s][t] = tmp[t];
+    }
+    const fftc_status st = setup_gpass(p, Lj, pj, R, S);
+    return st == FFTC_SUCCESS ? p : fail(p, st);
+  }
   if (Sj > 0) {
     // prime factors > 7: a kernel generated for N and compiled now (NVRTC, sm_100a)
     if (!jit_available()) return fail(p, FFTC_ERROR_UNSUPPORTED_SIZE);
@@ -339,7 +365,10 @@ fftc_plan* fftc_plan_create(int64_t N, int64_t batch, int sign) {
     const int pg = gpass_split(N, Lg, kMaxGPasses);
     if (pg < 0) return fail(p, FFTC_ERROR_UNSUPPORTED_SIZE);
     int R[kMaxGPasses][kMaxStages], S[kMaxGPasses];
-    for (int s = 0; s < pg; ++s) S[s] = generic_radices(Lg[s], R[s], kMaxStages);
+    const char* ej = getenv("FFTC_GPASS_JIT");
+    const bool jit = jit_available() && !(ej && strcmp(ej, "0") == 0);
+    for (int s = 0; s < pg; ++s)  // JIT passes: balanced radices; compiled kernel: the generic set
+      S[s] = jit ? jit_pass_radices(Lg[s], R[s], kMaxStages) : generic_radices(Lg[s], R[s], kMaxStages);
     const fftc_status st = setup_gpass(p, Lg, pg, R, S);
     return st == FFTC_SUCCESS ? p : fail(p, st);
   }
@@ -516,7 +545,7 @@ int fftc_plan_describe(const fftc_plan* p, char* buf, size_t len) {
       for (int s = 0; s < p->gp.p; ++s) {
         n += snprintf(tmp + n, sizeof(tmp) - n, "%s%d(", s ? "," : "", p->gp.st[s].L);
         rad(p->gp.st[s].R, p->gp.st[s].S);
-        n += snprintf(tmp + n, sizeof(tmp) - n, ")");
+        n += snprintf(tmp + n, sizeof(tmp) - n, ")%s", p->gp.st[s].jk ? "jit" : "");
       }
       n += snprintf(tmp + n, sizeof(tmp) - n, " workspace=%lld launches=%d",
                     (long long)(p->gp.p > 1 ? p->N * p->batch * (int64_t)sizeof(float2) : 0), p->gp.p);
@@ -680,6 +709,19 @@ int fftc_jit_compile(int64_t N, char* log, size_t loglen) {
   if (N < 2 || N > kGenericMaxN) return -1;
   std::string cubin, lg;
   const int rc = jit_compile_cubin((int)N, &cubin, &lg);
+  if (log && loglen) {
+    strncpy(log, lg.c_str(), loglen - 1);
+    log[loglen - 1] = 0;
+  }
+  return rc == 0 ? (int)cubin.size() : rc;
+}
+
+int fftc_jit_pass_compile(int L, char* log, size_t loglen) {
+  int R[32];
+  const int S = jit_pass_radices(L, R, 32);
+  if (L < 2 || L > kGpassMaxL || S < 1) return -1;
+  std::string cubin, lg;
+  const int rc = jit_compile_src_public(jit_pass_source(L, R, S), &cubin, &lg);
   if (log && loglen) {
     strncpy(log, lg.c_str(), loglen - 1);
     log[loglen - 1] = 0;

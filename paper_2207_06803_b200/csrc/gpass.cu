@@ -117,15 +117,19 @@ __global__ void __launch_bounds__(kGpThreads, 4)
 
 }  // namespace
 
-int gpass_split(long long N, int* Ls, int max) {
+int gpass_split(long long N, int* Ls, int max, int max_prime) {
   if (N <= 4096) return -1;
   std::vector<int> f;
   long long n = N;
-  for (int p : {7, 5, 3, 2})
+  for (int p = max_prime; p >= 2; --p) {
+    bool prime = true;
+    for (int d = 2; d * d <= p; ++d) prime = prime && p % d;
+    if (!prime) continue;
     while (n % p == 0) {
       f.push_back(p);
       n /= p;
     }
+  }
   if (n != 1) return -1;
   // fewest passes: largest-first assignment of the prime factors to the group with the
   // smallest product, every group <= kGpassMaxL
@@ -175,7 +179,11 @@ cudaError_t gpass_execute(const GPassPlanData& d, const float2* in, float2* out,
     const int tiles = (int)((NB + cols - 1) / cols);
     const long long grid = batch * tiles;
     if (grid > 0x7fffffffLL) return cudaErrorInvalidValue;
-    if (grid > 0) {
+    if (g.jk) {  // the pass specialised to (L, radices) by NVRTC
+      cudaError_t e = jit_pass_launch(g.jk, src, dst, g.tw, g.twA, g.twB, d.N, g.Ns, g.tws, batch,
+                                      conj && s == 0, conj && s == d.p - 1, st);
+      if (e != cudaSuccess) return e;
+    } else if (grid > 0) {
       const size_t smem = (size_t)2 * cols * (g.L + 1) * sizeof(float2);
       k_gpass<<<(unsigned)grid, kGpThreads, smem, st>>>(src, dst, g, d.N, tiles, (conj && s == 0) ? -1.f : 1.f,
                                                           (conj && s == d.p - 1) ? -1.f : 1.f);

@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include "jit.h"
 #include "registry.h"
 
 namespace fftc {
@@ -17,6 +18,7 @@ struct GPassStage {       // one pass (kernel argument)
   const float2* twA;      // w_{Ns L}^t, t < 2^tws
   const float2* twB;      // w_{Ns L}^{2^tws h}
   int tws;                // balanced table split (both tables L1-resident)
+  const JitKernel* jk;    // NVRTC kernel specialised to (L, radices), or null: k_gpass
 };
 
 struct GPassPlanData {
@@ -25,9 +27,10 @@ struct GPassPlanData {
   GPassStage st[kMaxGPasses] = {};
 };
 
-// Pass lengths for a 7-smooth N > 4096: the fewest passes (2..max) with every length
+// Pass lengths for an N > 4096 whose prime factors are <= max_prime (7: compiled codelets;
+// up to kJitMaxPrime with JIT pass kernels): the fewest passes (2..max) with every length
 // <= kGpassMaxL, longest first.  Returns p or -1.
-int gpass_split(long long N, int* Ls, int max);
+int gpass_split(long long N, int* Ls, int max, int max_prime = 7);
 cudaError_t gpass_execute(const GPassPlanData& d, const float2* in, float2* out, float2* work, long long batch,
                           int conj, cudaStream_t st);
 

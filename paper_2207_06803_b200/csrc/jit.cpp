@@ -207,53 +207,60 @@ int jit_radices(int N, int* R, int max) {
   return (int)out.size();
 }
 
+int jit_pass_radices(int L, int* R, int max) {
+  std::vector<int> f;
+  int n = L;
+  for (int p = 2; p <= n; ++p)
+    while (n % p == 0) {
+      if (p > kJitMaxPrime) return -1;
+      f.push_back(p);
+      n /= p;
+    }
+  // balanced groups (fewest stages with every radix <= 32, or a lone prime): more butterflies
+  // per stage than peeling 16s/25s off, e.g. 100 -> 10 x 10 instead of 4 x 25
+  for (int g = 1; g <= 4; ++g) {
+    std::vector<int> grp((size_t)g, 1);
+    for (size_t i = f.size(); i-- > 0;) {  // largest primes first, onto the smallest group
+      size_t best = 0;
+      for (size_t j = 1; j < grp.size(); ++j)
+        if (grp[j] < grp[best]) best = j;
+      grp[best] *= f[i];
+    }
+    bool ok = true;
+    for (int x : grp) ok = ok && (x <= 32 || (x <= kJitMaxPrime && smallest_prime(x) == x));
+    if (!ok && g < 4) continue;
+    if (g > max) return -1;
+    int S = 0;
+    for (int x : grp)
+      if (x > 1) R[S++] = x;
+    return S;
+  }
+  return -1;
+}
+
 int jit_fpb(int N) {
   int f = kJitTile / N;
   return f < 1 ? 1 : f;
 }
 
-std::string jit_source(int N) {
-  int R[32];
-  const int S = jit_radices(N, R, 32);
-  if (S < 0) return "";
-  const int FPB = jit_fpb(N), NP = N | 1;
-  std::string s;
-  s += "// generated by libfftc (jit.cpp) for N = " + std::to_string(N) + "\n";
-  s += "struct alignas(8) cf { float x, y; };\n";
-  std::vector<int> done;
-  for (int i = 0; i < S; ++i) {
-    bool seen = false;
-    for (int d : done) seen = seen || d == R[i];
-    if (seen) continue;
-    done.push_back(R[i]);
-    s += codelet_fn(R[i]);
-  }
-  char b[512];
-  snprintf(b, sizeof b,
-           "extern \"C\" __global__ void __launch_bounds__(%d) fftc_jit(const cf* __restrict__ in, cf* __restrict__ out,\n"
-           "    const cf* __restrict__ tw, long long batch, float csign) {\n"
-           "  extern __shared__ cf sm[];\n"
-           "  constexpr int N = %d, FPB = %d, NP = %d, T = %d;\n",
-           kJitThreads, N, FPB, NP, kJitThreads);
-  s += b;
-  s += "  const long long f0 = (long long)blockIdx.x * FPB;\n"
-       "  const int nf = (int)(batch - f0 < FPB ? batch - f0 : FPB);\n"
-       "  cf* A = sm; cf* B = sm + FPB * NP;\n"
-       "  const cf* gi = in + f0 * N; cf* go = out + f0 * N;\n"
-       "  for (int e = threadIdx.x; e < nf * N; e += T) { const cf a = gi[e]; A[(e / N) * NP + e % N] = cf{a.x, csign * a.y}; }\n"
-       "  __syncthreads();\n";
+namespace {
+
+// Stockham sub-stages of DFT_L over `count` rows (transforms / columns) held at pitch P in
+// shared memory, ping-ponging between A and B (one level of Eq. 2 per stage); twiddles from
+// the stage table `tw` (entry (Ns-1) + (r-1) Ns + m = w^{m r}).
+void emit_stages(std::string& s, int L, const int* R, int S, const char* count, int P) {
+  char b[640];
   int Ns = 1;
   for (int i = 0; i < S; ++i) {
-    const int Rs = R[i], NB = N / Rs;
+    const int Rs = R[i], NB = L / Rs;
     snprintf(b, sizeof b,
-             "  { // stage %d: radix %d, Ns %d\n"
-             "    for (int q = threadIdx.x; q < nf * %d; q += T) {\n"
+             "  { // sub-stage %d: radix %d, Ns %d\n"
+             "    for (int q = threadIdx.x; q < (%s) * %d; q += T) {\n"
              "      const int f = q / %d, j = q %% %d, m = j %% %d;\n"
-             "      const cf* a = A + f * NP; cf* bb = B + f * NP;\n"
-             "      cf v[%d];\n",
-             i, Rs, Ns, NB, NB, NB, Ns, Rs);
-    s += b;
-    snprintf(b, sizeof b, "      for (int r = 0; r < %d; ++r) v[r] = a[j + r * %d];\n", Rs, NB);
+             "      const cf* a = A + f * %d; cf* bb = B + f * %d;\n"
+             "      cf v[%d];\n"
+             "      for (int r = 0; r < %d; ++r) v[r] = a[j + r * %d];\n",
+             i, Rs, Ns, count, NB, NB, NB, Ns, P, P, Rs, Rs, NB);
     s += b;
     if (Ns > 1) {
       snprintf(b, sizeof b,
@@ -273,7 +280,108 @@ std::string jit_source(int N) {
     s += b;
     Ns *= Rs;
   }
+}
+
+std::string prelude(const int* R, int S) {
+  std::string s = "struct alignas(8) cf { float x, y; };\n";
+  std::vector<int> done;
+  for (int i = 0; i < S; ++i) {
+    bool seen = false;
+    for (int d : done) seen = seen || d == R[i];
+    if (seen) continue;
+    done.push_back(R[i]);
+    s += codelet_fn(R[i]);
+  }
+  return s;
+}
+
+}  // namespace
+
+std::string jit_source(int N) {
+  int R[32];
+  const int S = jit_radices(N, R, 32);
+  if (S < 0) return "";
+  const int FPB = jit_fpb(N), NP = N | 1;
+  std::string s = "// generated by libfftc (jit.cpp) for N = " + std::to_string(N) + "\n" + prelude(R, S);
+  char b[512];
+  snprintf(b, sizeof b,
+           "extern \"C\" __global__ void __launch_bounds__(%d) fftc_jit(const cf* __restrict__ in, cf* __restrict__ out,\n"
+           "    const cf* __restrict__ tw, long long batch, float csign) {\n"
+           "  extern __shared__ cf sm[];\n"
+           "  constexpr int N = %d, FPB = %d, NP = %d, T = %d;\n",
+           kJitThreads, N, FPB, NP, kJitThreads);
+  s += b;
+  s += "  const long long f0 = (long long)blockIdx.x * FPB;\n"
+       "  const int nf = (int)(batch - f0 < FPB ? batch - f0 : FPB);\n"
+       "  cf* A = sm; cf* B = sm + FPB * NP;\n"
+       "  const cf* gi = in + f0 * N; cf* go = out + f0 * N;\n"
+       "  for (int e = threadIdx.x; e < nf * N; e += T) { const cf a = gi[e]; A[(e / N) * NP + e % N] = cf{a.x, csign * a.y}; }\n"
+       "  __syncthreads();\n";
+  emit_stages(s, N, R, S, "nf", NP);
   s += "  for (int e = threadIdx.x; e < nf * N; e += T) { const cf a = A[(e / N) * NP + e % N]; go[e] = cf{a.x, csign * a.y}; }\n"
+       "}\n";
+  return s;
+}
+
+int jit_pass_cols(int L) {
+  int c = 16;
+  while (c < 256 && 2 * c * L <= 4096) c *= 2;
+  return c;
+}
+
+// One pass of the runtime multi-pass path (the kernel of gpass.cu) with L, its radices and
+// the column count compiled in: straight-line codelets (any prime up to kJitMaxPrime),
+// constant-divisor index math.  Ns, the twiddle split and the sizes stay runtime arguments,
+// so one kernel serves every pass of that length.
+std::string jit_pass_source(int L, const int* R, int S) {
+  const int LP = L + 1, COLS = jit_pass_cols(L);
+  int LC = 0;
+  while ((1 << LC) < COLS) ++LC;
+  std::string s = "// generated by libfftc (jit.cpp): pass of length " + std::to_string(L) + "\n" + prelude(R, S);
+  char b[900];
+  snprintf(b, sizeof b,
+           "extern \"C\" __global__ void __launch_bounds__(%d, 4) fftc_jit_pass(const cf* __restrict__ in,\n"
+           "    cf* __restrict__ out, const cf* __restrict__ tw, const cf* __restrict__ twA, const cf* __restrict__ twB,\n"
+           "    long long N, int Ns, int tws, int tiles, float csign_in, float csign_out) {\n"
+           "  extern __shared__ cf sm[];\n"
+           "  constexpr int L = %d, LP = %d, COLS = %d, LC = %d, T = %d;\n"
+           "  __shared__ int s_cq[COLS], s_cm[COLS];\n",
+           kJitThreads, L, LP, COLS, LC, kJitThreads);
+  s += b;
+  s += "  const long long NB = N / L;\n"
+       "  const long long bt = blockIdx.x / tiles;\n"
+       "  const long long c0 = (long long)(blockIdx.x % tiles) * COLS;\n"
+       "  const int nc = (int)(NB - c0 < COLS ? NB - c0 : COLS);\n"
+       "  cf* A = sm; cf* B = sm + COLS * LP;\n"
+       "  for (int f = threadIdx.x; f < COLS; f += T) { const int c = (int)c0 + f; s_cq[f] = c / Ns; s_cm[f] = c - (c / Ns) * Ns; }\n"
+       "  __syncthreads();\n"
+       "  const cf* gi = in + bt * N + c0;\n"
+       "  const long long amask = (1LL << tws) - 1;\n"
+       "  for (int e0 = threadIdx.x; e0 < (L << LC); e0 += 8 * T) {\n"
+       "    cf v[8];\n"
+       "#pragma unroll\n"
+       "    for (int u = 0; u < 8; ++u) { const int e = e0 + u * T, f = e & (COLS - 1), r = e >> LC;\n"
+       "      v[u] = (e < (L << LC) && f < nc) ? gi[f + (long long)r * NB] : cf{0.f, 0.f}; }\n"
+       "#pragma unroll\n"
+       "    for (int u = 0; u < 8; ++u) { const int e = e0 + u * T, f = e & (COLS - 1), r = e >> LC;\n"
+       "      if (e < (L << LC) && f < nc) { cf x = v[u]; x.y *= csign_in;\n"
+       "        if (Ns > 1) { const long long ex = (long long)s_cm[f] * r;\n"
+       "          const cf p = twA[ex & amask], q = twB[ex >> tws];\n"
+       "          const cf w = cf{fmaf(p.x, q.x, -p.y * q.y), fmaf(p.x, q.y, p.y * q.x)};\n"
+       "          x = cf{fmaf(x.x, w.x, -x.y * w.y), fmaf(x.x, w.y, x.y * w.x)}; }\n"
+       "        A[f * LP + r] = x; } }\n"
+       "  }\n"
+       "  __syncthreads();\n";
+  emit_stages(s, L, R, S, "nc", LP);
+  s += "  cf* go = out + bt * N;\n"
+       "  if (Ns == 1) {\n"
+       "    for (int e = threadIdx.x; e < nc * L; e += T) { const int f = e / L, r = e - (e / L) * L;\n"
+       "      const cf a = A[f * LP + r]; go[(c0 + f) * L + r] = cf{a.x, csign_out * a.y}; }\n"
+       "  } else {\n"
+       "    for (int e = threadIdx.x; e < (L << LC); e += T) { const int f = e & (COLS - 1), r = e >> LC;\n"
+       "      if (f < nc) { const cf a = A[f * LP + r];\n"
+       "        go[((long long)s_cq[f] * L + r) * Ns + s_cm[f]] = cf{a.x, csign_out * a.y}; } }\n"
+       "  }\n"
        "}\n";
   return s;
 }
@@ -328,17 +436,12 @@ F driver_fn(const char* name) {
 }
 
 std::mutex g_mu;
-std::map<int, JitKernel*> g_cache;
+std::map<std::string, JitKernel*> g_cache;
 std::string g_log;
 
-}  // namespace
-
-bool jit_available() { return nvrtc().ok; }
-
-int jit_compile_cubin(int N, std::string* cubin, std::string* log) {
+int compile_src(const std::string& src, std::string* cubin, std::string* log) {
   const Nvrtc& n = nvrtc();
   if (!n.ok) return -1;
-  const std::string src = jit_source(N);
   if (src.empty()) return -2;
   void* prog = nullptr;
   if (n.create(&prog, src.c_str(), "fftc_jit.cu", 0, nullptr, nullptr) != 0) return -3;
@@ -362,10 +465,15 @@ int jit_compile_cubin(int N, std::string* cubin, std::string* log) {
   return 0;
 }
 
-const JitKernel* jit_get(int N, cudaError_t* err) {
+// Compile + load `src`, kernel `name`, dynamic shared memory `smem`; cached under `key`.
+const JitKernel* load_kernel(const std::string& key, const std::string& src, const char* name, size_t smem, int N,
+                             int fpb, cudaError_t* err) {
   std::lock_guard<std::mutex> lk(g_mu);
-  auto it = g_cache.find(N);
-  if (it != g_cache.end()) return it->second;
+  auto it = g_cache.find(key);
+  if (it != g_cache.end()) {
+    *err = cudaSuccess;
+    return it->second;
+  }
   typedef CUresult (*load_t)(CUmodule*, const void*);
   typedef CUresult (*getfn_t)(CUfunction*, CUmodule, const char*);
   typedef CUresult (*setattr_t)(CUfunction, CUfunction_attribute, int);
@@ -379,26 +487,68 @@ const JitKernel* jit_get(int N, cudaError_t* err) {
   if (*err != cudaSuccess) return nullptr;
   *err = cudaErrorNotSupported;
   std::string cubin;
-  if (jit_compile_cubin(N, &cubin, &g_log) != 0) return nullptr;
+  if (compile_src(src, &cubin, &g_log) != 0) return nullptr;
   CUmodule mod = nullptr;
   CUfunction fn = nullptr;
-  if (load(&mod, cubin.data()) != CUDA_SUCCESS || getfn(&fn, mod, "fftc_jit") != CUDA_SUCCESS) {
+  if (load(&mod, cubin.data()) != CUDA_SUCCESS || getfn(&fn, mod, name) != CUDA_SUCCESS) {
     *err = cudaErrorInvalidKernelImage;
     return nullptr;
   }
   JitKernel* k = new JitKernel();
   k->fn = fn;
   k->N = N;
-  k->fpb = jit_fpb(N);
-  k->smem = (size_t)2 * k->fpb * (N | 1) * 8;
+  k->fpb = fpb;
+  k->smem = smem;
   if (setattr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)k->smem) != CUDA_SUCCESS) {
     delete k;
     *err = cudaErrorInvalidValue;
     return nullptr;
   }
-  g_cache[N] = k;
+  g_cache[key] = k;
   *err = cudaSuccess;
   return k;
+}
+
+}  // namespace
+
+bool jit_available() { return nvrtc().ok; }
+
+int jit_compile_cubin(int N, std::string* cubin, std::string* log) { return compile_src(jit_source(N), cubin, log); }
+
+int jit_compile_src_public(const std::string& src, std::string* cubin, std::string* log) {
+  return compile_src(src, cubin, log);
+}
+
+const JitKernel* jit_get(int N, cudaError_t* err) {
+  const int fpb = jit_fpb(N);
+  return load_kernel("n:" + std::to_string(N), jit_source(N), "fftc_jit", (size_t)2 * fpb * (N | 1) * 8, N, fpb, err);
+}
+
+const JitKernel* jit_pass_get(int L, const int* R, int S, cudaError_t* err) {
+  std::string key = "p:" + std::to_string(L);
+  for (int i = 0; i < S; ++i) key += ":" + std::to_string(R[i]);
+  const int cols = jit_pass_cols(L);
+  return load_kernel(key, jit_pass_source(L, R, S), "fftc_jit_pass", (size_t)2 * cols * (L + 1) * 8, L, cols, err);
+}
+
+cudaError_t jit_pass_launch(const JitKernel* k, const float2* in, float2* out, const float2* tw, const float2* twA,
+                            const float2* twB, long long N, int Ns, int tws, long long batch, int conj_in,
+                            int conj_out, cudaStream_t st) {
+  typedef CUresult (*launch_t)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
+                               CUstream, void**, void**);
+  static launch_t launch = driver_fn<launch_t>("cuLaunchKernel");
+  if (!launch) return cudaErrorNotSupported;
+  const long long NB = N / k->N;
+  int tiles = (int)((NB + k->fpb - 1) / k->fpb);
+  const long long grid = batch * tiles;
+  if (grid == 0) return cudaSuccess;
+  if (grid > 0x7fffffffLL) return cudaErrorInvalidValue;
+  float ci = conj_in ? -1.f : 1.f, co = conj_out ? -1.f : 1.f;
+  void* args[] = {(void*)&in, (void*)&out, (void*)&tw, (void*)&twA, (void*)&twB, (void*)&N, (void*)&Ns,
+                  (void*)&tws, (void*)&tiles, (void*)&ci, (void*)&co};
+  const CUresult r = launch(k->fn, (unsigned)grid, 1, 1, kJitThreads, 1, 1, (unsigned)k->smem, (CUstream)st, args,
+                            nullptr);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorLaunchFailure;
 }
 
 cudaError_t jit_launch(const JitKernel* k, const float2* in, float2* out, const float2* tw, long long batch, int conj,

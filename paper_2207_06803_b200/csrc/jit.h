@@ -22,15 +22,27 @@ struct JitKernel {
 // or -1 if N has a prime factor > kJitMaxPrime.
 int jit_radices(int N, int* R, int max);
 int jit_fpb(int N);
+// Radices of a JIT pass kernel of length L: balanced groups of its prime factors.
+int jit_pass_radices(int L, int* R, int max);
 // CUDA C++ source of the kernel specialised to N ("" if unsupported).
 std::string jit_source(int N);
 // NVRTC compile to an sm_100a cubin (no device needed).  0 on success.
 int jit_compile_cubin(int N, std::string* cubin, std::string* log);
+int jit_compile_src_public(const std::string& src, std::string* cubin, std::string* log);
 bool jit_available();
 // Compiled + loaded kernel for N (cached per process).
 const JitKernel* jit_get(int N, cudaError_t* err);
 cudaError_t jit_launch(const JitKernel* k, const float2* in, float2* out, const float2* tw, long long batch, int conj,
                        cudaStream_t st);
 const char* jit_last_log();
+
+// One pass of the runtime multi-pass path (gpass.cu) specialised to its length L and radices
+// (any primes up to kJitMaxPrime), compiled by NVRTC and cached per (L, radices).
+int jit_pass_cols(int L);
+std::string jit_pass_source(int L, const int* R, int S);
+const JitKernel* jit_pass_get(int L, const int* R, int S, cudaError_t* err);
+cudaError_t jit_pass_launch(const JitKernel* k, const float2* in, float2* out, const float2* tw, const float2* twA,
+                            const float2* twB, long long N, int Ns, int tws, long long batch, int conj_in,
+                            int conj_out, cudaStream_t st);
 
 }  // namespace fftc

@@ -152,6 +152,6 @@ def test_invalid_args_before_device():
     assert fftc.fftc_last_error() == fftc.FFTC_ERROR_INVALID_VALUE
     assert fftc.fftc_plan_create(67, 1, -1) == 0  # prime > 61: neither compiled nor JIT codelets
     assert fftc.fftc_last_error() == fftc.FFTC_ERROR_UNSUPPORTED_SIZE
-    assert fftc.fftc_plan_create(11 * 4096, 1, -1) == 0  # prime > 7 above the single-pass limit
+    assert fftc.fftc_plan_create(67 * 4096, 1, -1) == 0  # prime > 61 above the single-pass limit
     assert fftc.fftc_last_error() == fftc.FFTC_ERROR_UNSUPPORTED_SIZE
     assert fftc.fftc_execute(0, 0, 0, 0) == fftc.FFTC_ERROR_INVALID_VALUE

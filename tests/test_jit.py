@@ -26,13 +26,19 @@ def test_jit_source_compiles_for_sm100a(N):
     assert r > 0, log
 
 
+@pytest.mark.parametrize("L", [11, 61, 100, 125, 143, 243, 256, 2 * 61])
+def test_jit_pass_source_compiles_for_sm100a(L):
+    r, log = fftc.fftc_jit_pass_compile(L)
+    assert r > 0, log
+
+
 def test_jit_planner_domain():
     for N in JIT_SIZES:
         assert _jit(N), N
     assert not _jit(67)            # prime above 61
     assert not _jit(64 * 67)
     assert not _jit(1)
-    assert fftc.fftc_jit_source(4096 * 11) is None  # above the single-pass limit
+    assert fftc.fftc_jit_source(4096 * 11) is None  # above the single-pass limit (runtime passes)
 
 
 def test_generated_codelet_source_shape():
@@ -60,7 +66,44 @@ def test_gpu_jit_parity(N):
 @pytest.mark.gpu
 def test_gpu_jit_unsupported():
     pytest.importorskip("torch")
-    for N in (67, 64 * 67, 4096 * 11):
+    for N in (67, 64 * 67, 4096 * 67):
         with pytest.raises(fftc.FFTCError) as e:
             fftc.Plan(N, 2, -1)
         assert e.value.status == fftc.FFTC_ERROR_UNSUPPORTED_SIZE
+
+
+LARGE_JIT = [(11 * 4096, 3), (13 * 13 * 256, 3), (61 * 1024, 2), (11 * 13 * 17 * 19, 2), (3 ** 5 * 59, 4),
+             (11 * (1 << 16), 1)]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N,batch", LARGE_JIT)
+def test_gpu_jit_large_passes(N, batch):
+    """N > 4096 with prime factors 11..61: runtime passes, each an NVRTC kernel specialised to
+    its length (any radix from the emitter), both signs, against the oracle."""
+    torch = pytest.importorskip("torch")
+    x = synth.uniform_c64(N, batch, seed=N % 997)
+    for sign in (-1, 1):
+        with fftc.Plan(N, batch, sign) as p:
+            assert "kind=gpass" in p.describe() and "jit" in p.describe(), p.describe()
+            y = p(torch.from_numpy(x).cuda())
+            torch.cuda.synchronize()
+            y = y.cpu().numpy()
+        err = oracle.rel_l2(y, oracle.fft_ct(x, sign)).max()
+        assert err <= min(oracle.tolerance(N), 2e-6), (N, sign, err)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N", [12288, 59049, 100000])
+def test_gpu_gpass_compiled_kernel_without_jit(N, monkeypatch):
+    """FFTC_GPASS_JIT=0: the compiled runtime-schedule pass kernel (k_gpass) stays correct."""
+    torch = pytest.importorskip("torch")
+    monkeypatch.setenv("FFTC_GPASS_JIT", "0")
+    x = synth.uniform_c64(N, 2, seed=N % 991)
+    with fftc.Plan(N, 2, -1) as p:
+        assert "kind=gpass" in p.describe() and "jit" not in p.describe(), p.describe()
+        y = p(torch.from_numpy(x).cuda())
+        torch.cuda.synchronize()
+        y = y.cpu().numpy()
+    err = oracle.rel_l2(y, oracle.fft_ct(x, -1)).max()
+    assert err <= min(oracle.tolerance(N), 2e-6), (N, err)
