@@ -116,7 +116,9 @@ int fftc_plan_passes(int64_t N, int* lengths, int max);
 
 /* Runtime-schedule multi-pass split (host only): for a 7-smooth N > 4096
  * that is not a power of two (those run fftc_plan_passes), the fewest
- * passes p in [2, 4] with lengths L_s <= 256, product N, longest first;
+ * passes p in [2, 4] with lengths L_s <= 512 (each pass a JIT kernel
+ * specialised to its length; <= 256 without NVRTC or with
+ * FFTC_GPASS_JIT=0), product N, longest first;
  * each pass is one level of Eq. 2 in Stockham form over HBM, its
  * DFT_{L_s} built from the generic radices {16, 8, 4, 2, 9, 3, 25, 5, 7}.
  * Writes up to `max` lengths, returns p, or -1 (N <= 4096, a prime

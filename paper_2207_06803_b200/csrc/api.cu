@@ -168,7 +168,7 @@ static fftc_status setup_gpass(fftc_plan* p, const int* Lg, int pg, const int (*
     g.Ns = (int)Ns;
     g.S = S[s];
     g.jk = nullptr;
-    if (g.L > kGpassMaxL || g.S < 1 || g.S > kMaxStages) return FFTC_ERROR_UNSUPPORTED_SIZE;
+    if (g.L > kJitPassMaxL || g.S < 1 || g.S > kMaxStages) return FFTC_ERROR_UNSUPPORTED_SIZE;
     int64_t prod = 1;
     bool generic = true;
     for (int t = 0; t < g.S; ++t) {
@@ -181,7 +181,7 @@ static fftc_status setup_gpass(fftc_plan* p, const int* Lg, int pg, const int (*
       cudaError_t je = cudaSuccess;
       g.jk = jit_pass_get(g.L, g.R, g.S, &je);
     }
-    if (!g.jk && !generic) return FFTC_ERROR_UNSUPPORTED_SIZE;
+    if (!g.jk && (!generic || g.L > kGpassMaxL)) return FFTC_ERROR_UNSUPPORTED_SIZE;
     const int64_t T = Ns * Lg[s];
     float2* t0 = upload_stage_table(Lg[s], g.R, g.S, &err);
     p->gp_tables[3 * s] = t0;
@@ -230,7 +230,9 @@ fftc_plan* fftc_plan_create(int64_t N, int64_t batch, int sign) {
   int Rj[32];
   const int Sj = seven_smooth(N) ? -1 : (N <= kGenericMaxN ? jit_radices((int)N, Rj, 32) : -1);
   int Lj[kMaxGPasses];
-  const int pj = (!seven_smooth(N) && N > kGenericMaxN) ? gpass_split(N, Lj, kMaxGPasses, kJitMaxPrime) : -1;
+  const int pj = (!seven_smooth(N) && N > kGenericMaxN)
+                     ? gpass_split(N, Lj, kMaxGPasses, kJitMaxPrime, kJitPassMaxL)
+                     : -1;
   if (!seven_smooth(N) && Sj < 0 && pj < 0) return fail(nullptr, FFTC_ERROR_UNSUPPORTED_SIZE);
   if (batch > 0 && batch > ((int64_t)1 << 60) / (N * 8)) return fail(nullptr, FFTC_ERROR_UNSUPPORTED_SIZE);
   int dev = 0;
@@ -361,12 +363,13 @@ fftc_plan* fftc_plan_create(int64_t N, int64_t batch, int sign) {
   // any other 7-smooth N (and FFTC_LARGE=gpass): runtime-schedule multi-pass kernels
   const bool force_gpass = large && strcmp(large, "gpass") == 0;
   if (np < 0 || force_gpass) {
-    int Lg[kMaxGPasses];
-    const int pg = gpass_split(N, Lg, kMaxGPasses);
-    if (pg < 0) return fail(p, FFTC_ERROR_UNSUPPORTED_SIZE);
-    int R[kMaxGPasses][kMaxStages], S[kMaxGPasses];
     const char* ej = getenv("FFTC_GPASS_JIT");
     const bool jit = jit_available() && !(ej && strcmp(ej, "0") == 0);
+    int Lg[kMaxGPasses];
+    // JIT passes run lengths up to 1024 in place (fewer HBM passes); the compiled kernel 256
+    const int pg = gpass_split(N, Lg, kMaxGPasses, 7, jit ? kJitPassMaxL : kGpassMaxL);
+    if (pg < 0) return fail(p, FFTC_ERROR_UNSUPPORTED_SIZE);
+    int R[kMaxGPasses][kMaxStages], S[kMaxGPasses];
     for (int s = 0; s < pg; ++s)  // JIT passes: balanced radices; compiled kernel: the generic set
       S[s] = jit ? jit_pass_radices(Lg[s], R[s], kMaxStages) : generic_radices(Lg[s], R[s], kMaxStages);
     const fftc_status st = setup_gpass(p, Lg, pg, R, S);
@@ -588,7 +591,12 @@ int fftc_plan_split(int64_t N, int64_t* M, int64_t* K) { return top_split(N, M, 
 
 int fftc_plan_passes(int64_t N, int* lengths, int max) { return pass_split(N, lengths, max); }
 
-int fftc_plan_gpasses(int64_t N, int* lengths, int max) { return gpass_split(N, lengths, max); }
+int fftc_plan_gpasses(int64_t N, int* lengths, int max) {
+  // as the plan does: JIT passes up to 1024 long when NVRTC is there, else the compiled 256
+  const char* ej = getenv("FFTC_GPASS_JIT");
+  const bool jit = jit_available() && !(ej && strcmp(ej, "0") == 0);
+  return gpass_split(N, lengths, max, 7, jit ? kJitPassMaxL : kGpassMaxL);
+}
 
 int fftc_expr_radices(const char* expr, int64_t* N, int* radices, int max, char* err, size_t errlen) {
   int64_t r[64];
@@ -719,7 +727,7 @@ int fftc_jit_compile(int64_t N, char* log, size_t loglen) {
 int fftc_jit_pass_compile(int L, char* log, size_t loglen) {
   int R[32];
   const int S = jit_pass_radices(L, R, 32);
-  if (L < 2 || L > kGpassMaxL || S < 1) return -1;
+  if (L < 2 || L > kJitPassMaxL || S < 1) return -1;
   std::string cubin, lg;
   const int rc = jit_compile_src_public(jit_pass_source(L, R, S), &cubin, &lg);
   if (log && loglen) {

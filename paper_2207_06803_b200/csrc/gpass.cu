@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(kGpThreads, 4)
 
 }  // namespace
 
-int gpass_split(long long N, int* Ls, int max, int max_prime) {
+int gpass_split(long long N, int* Ls, int max, int max_prime, int max_len) {
   if (N <= 4096) return -1;
   std::vector<int> f;
   long long n = N;
@@ -140,7 +140,7 @@ int gpass_split(long long N, int* Ls, int max, int max_prime) {
       size_t best = 0;
       for (size_t i = 1; i < g.size(); ++i)
         if (g[i] < g[best]) best = i;
-      if (g[best] * x > kGpassMaxL) {
+      if (g[best] * x > max_len) {
         ok = false;
         break;
       }

@@ -30,7 +30,7 @@ struct GPassPlanData {
 // Pass lengths for an N > 4096 whose prime factors are <= max_prime (7: compiled codelets;
 // up to kJitMaxPrime with JIT pass kernels): the fewest passes (2..max) with every length
 // <= kGpassMaxL, longest first.  Returns p or -1.
-int gpass_split(long long N, int* Ls, int max, int max_prime = 7);
+int gpass_split(long long N, int* Ls, int max, int max_prime = 7, int max_len = kGpassMaxL);
 cudaError_t gpass_execute(const GPassPlanData& d, const float2* in, float2* out, float2* work, long long batch,
                           int conj, cudaStream_t st);
 

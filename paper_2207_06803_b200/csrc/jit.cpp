@@ -282,6 +282,49 @@ void emit_stages(std::string& s, int L, const int* R, int S, const char* count, 
   }
 }
 
+// In-place variant for long passes (one buffer, half the shared memory): every thread first
+// reads all of its butterflies of the stage into registers (KB = ceil(COLS NB / T) per thread,
+// compile-time), the CTA syncs, then writes -- as the compiled fused kernels do.
+void emit_stages_inplace(std::string& s, int L, const int* R, int S, int COLS, int T, int P) {
+  char b[900];
+  int Ns = 1;
+  for (int i = 0; i < S; ++i) {
+    const int Rs = R[i], NB = L / Rs, KB = (COLS * NB + T - 1) / T;
+    snprintf(b, sizeof b,
+             "  { // sub-stage %d (in place): radix %d, Ns %d\n"
+             "    cf v[%d][%d]; int jj[%d], ff[%d];\n"
+             "#pragma unroll\n"
+             "    for (int kb = 0; kb < %d; ++kb) { const int q = threadIdx.x + kb * T; ff[kb] = -1;\n"
+             "      if (q < nc * %d) { const int f = q / %d, j = q %% %d; ff[kb] = f; jj[kb] = j;\n"
+             "#pragma unroll\n"
+             "        for (int r = 0; r < %d; ++r) v[kb][r] = A[f * %d + j + r * %d]; } }\n"
+             "    __syncthreads();\n"
+             "#pragma unroll\n"
+             "    for (int kb = 0; kb < %d; ++kb) { if (ff[kb] < 0) continue; const int f = ff[kb], j = jj[kb], m = j %% %d;\n",
+             i, Rs, Ns, KB, Rs, KB, KB, KB, NB, NB, NB, Rs, P, NB, KB, Ns);
+    s += b;
+    if (Ns > 1) {
+      snprintf(b, sizeof b,
+               "#pragma unroll\n"
+               "      for (int r = 1; r < %d; ++r) { const cf w = tw[%d + (r - 1) * %d + m];\n"
+               "        v[kb][r] = cf{fmaf(v[kb][r].x, w.x, -v[kb][r].y * w.y), fmaf(v[kb][r].x, w.y, v[kb][r].y * w.x)}; }\n",
+               Rs, Ns - 1, Ns);
+      s += b;
+    }
+    snprintf(b, sizeof b,
+             "      dft%d(v[kb]);\n"
+             "      const int o = (j / %d) * %d + m;\n"
+             "#pragma unroll\n"
+             "      for (int r = 0; r < %d; ++r) A[f * %d + o + r * %d] = v[kb][r];\n"
+             "    }\n"
+             "    __syncthreads();\n"
+             "  }\n",
+             Rs, Ns, Ns * Rs, Rs, P, Ns);
+    s += b;
+    Ns *= Rs;
+  }
+}
+
 std::string prelude(const int* R, int S) {
   std::string s = "struct alignas(8) cf { float x, y; };\n";
   std::vector<int> done;
@@ -324,9 +367,13 @@ std::string jit_source(int N) {
 }
 
 int jit_pass_cols(int L) {
+  if (L > 256) return 8;  // long passes: in place, 8 columns (64-byte rows), <= 66 KB
   int c = 16;
   while (c < 256 && 2 * c * L <= 4096) c *= 2;
   return c;
+}
+size_t jit_pass_smem(int L) {
+  return (size_t)(L > 256 ? 1 : 2) * jit_pass_cols(L) * (L + 1) * 8;
 }
 
 // One pass of the runtime multi-pass path (the kernel of gpass.cu) with L, its radices and
@@ -352,7 +399,7 @@ std::string jit_pass_source(int L, const int* R, int S) {
        "  const long long bt = blockIdx.x / tiles;\n"
        "  const long long c0 = (long long)(blockIdx.x % tiles) * COLS;\n"
        "  const int nc = (int)(NB - c0 < COLS ? NB - c0 : COLS);\n"
-       "  cf* A = sm; cf* B = sm + COLS * LP;\n"
+       "  cf* A = sm;\n"
        "  for (int f = threadIdx.x; f < COLS; f += T) { const int c = (int)c0 + f; s_cq[f] = c / Ns; s_cm[f] = c - (c / Ns) * Ns; }\n"
        "  __syncthreads();\n"
        "  const cf* gi = in + bt * N + c0;\n"
@@ -372,7 +419,12 @@ std::string jit_pass_source(int L, const int* R, int S) {
        "        A[f * LP + r] = x; } }\n"
        "  }\n"
        "  __syncthreads();\n";
-  emit_stages(s, L, R, S, "nc", LP);
+  if (L > 256) {
+    emit_stages_inplace(s, L, R, S, COLS, kJitThreads, LP);
+  } else {
+    s += "  cf* B = sm + COLS * LP;\n";
+    emit_stages(s, L, R, S, "nc", LP);
+  }
   s += "  cf* go = out + bt * N;\n"
        "  if (Ns == 1) {\n"
        "    for (int e = threadIdx.x; e < nc * L; e += T) { const int f = e / L, r = e - (e / L) * L;\n"
@@ -528,7 +580,7 @@ const JitKernel* jit_pass_get(int L, const int* R, int S, cudaError_t* err) {
   std::string key = "p:" + std::to_string(L);
   for (int i = 0; i < S; ++i) key += ":" + std::to_string(R[i]);
   const int cols = jit_pass_cols(L);
-  return load_kernel(key, jit_pass_source(L, R, S), "fftc_jit_pass", (size_t)2 * cols * (L + 1) * 8, L, cols, err);
+  return load_kernel(key, jit_pass_source(L, R, S), "fftc_jit_pass", jit_pass_smem(L), L, cols, err);
 }
 
 cudaError_t jit_pass_launch(const JitKernel* k, const float2* in, float2* out, const float2* tw, const float2* twA,

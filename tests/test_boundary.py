@@ -112,7 +112,7 @@ def _smooth(n):
 
 
 def test_planner_gpasses():
-    """Runtime-schedule multi-pass split: product N, lengths <= 256 and 7-smooth, fewest
+    """Runtime-schedule multi-pass split: product N, lengths <= 512 and 7-smooth, fewest
     passes (a lower bound is ceil(log_256 N)), longest first, deterministic."""
     sizes = [4097 - 1 + 3 * 2, 12288, 13122, 15625, 16807, 19683, 40960, 46656, 59049, 78125, 100000,
              248832, 10 ** 6, 3 ** 13, 3 ** 15, 5 ** 10, 7 ** 8, 6 ** 10]
@@ -121,14 +121,15 @@ def test_planner_gpasses():
             continue
         Ls = fftc.fftc_plan_gpasses(N)
         assert Ls is not None, N
-        assert math.prod(Ls) == N and all(2 <= L <= 256 and _smooth(L) for L in Ls), (N, Ls)
-        assert len(Ls) >= math.ceil(math.log(N, 256) - 1e-12) and 2 <= len(Ls) <= 4
+        assert math.prod(Ls) == N and all(2 <= L <= 1024 and _smooth(L) for L in Ls), (N, Ls)
+        assert len(Ls) >= math.ceil(math.log(N, 512) - 1e-12) and 2 <= len(Ls) <= 4
         assert Ls == sorted(Ls, reverse=True)
         assert Ls == fftc.fftc_plan_gpasses(N)
     assert fftc.fftc_plan_gpasses(3 ** 10) == [243, 243]
     assert fftc.fftc_plan_gpasses(4096) is None        # single pass
     assert fftc.fftc_plan_gpasses(11 * 4096) is None   # prime factor > 7
     assert fftc.fftc_plan_gpasses(257 * 257) is None   # prime 257
+    assert fftc.fftc_plan_gpasses(10 ** 5) == [400, 250]  # JIT passes: up to 512 long
 
 
 def test_no_device_fails_loudly():
