@@ -41,8 +41,8 @@ typedef enum {
   FFTC_SUCCESS = 0,
   FFTC_ERROR_INVALID_VALUE = 1,    /* N < 1, batch < 0, sign not in {-1,+1}, NULL pointer,
                                       in == out or overlapping buffers */
-  FFTC_ERROR_UNSUPPORTED_SIZE = 2, /* N has a prime factor > 7 and is > 4096, or a prime factor > 61,
-                                      or NVRTC is unavailable for a JIT size; N*batch*8 overflows;
+  FFTC_ERROR_UNSUPPORTED_SIZE = 2, /* N has a prime factor > 61, or one > 7 and NVRTC is unavailable
+                                      (JIT sizes); N > 512^4; N*batch*8 overflows;
                                       dist: nranks does not divide M and K */
   FFTC_ERROR_MISALIGNED = 3,       /* in / out not 16-byte aligned */
   FFTC_ERROR_OUT_OF_MEMORY = 4,    /* twiddle table / workspace allocation failed */
