@@ -390,6 +390,98 @@ static cudaError_t launch_fused_batch(const float2* in, float2* out, const float
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- persistent register-pipelined kernel
+// LT_FAST direct schedules.  Each CTA loops over tiles of FPB transforms; the stage-0 inputs of
+// the CTA's NEXT tile are loaded into registers (plain coalesced loads, the same lanes and
+// elements stage 0 consumes) before the current tile's stages run, so every CTA keeps HBM
+// reads in flight while it computes instead of issuing them in one burst per tile.
+template <class P, int MINB>
+__global__ void __launch_bounds__(P::THREADS, MINB)
+    k_fused_pipe(const float2* __restrict__ in, float2* __restrict__ out, const float2* __restrict__ tw,
+                 long long batch, float csign) {
+  static_assert(P::MAP == LT_FAST, "register pipeline: LT_FAST mapping");
+  extern __shared__ float2 sm[];
+  constexpr int N = P::N, R = P::R(0), NB = N / R, KB = (NB + P::TPF - 1) / P::TPF;
+  constexpr bool EXACT = (NB % P::TPF) == 0;
+  int f, lt;
+  P::thread_coords(threadIdx.x, f, lt);
+  const long long ntiles = (batch + P::FPB - 1) / P::FPB;
+  float2 pre[KB][R];
+  auto fetch = [&](long long t) {
+    const long long tr = t * P::FPB + f;
+    if (t < ntiles && tr < batch) {
+      const float2* gi = in + tr * N;
+      sfor<KB>([&](auto k_) {
+        constexpr int k = decltype(k_)::value;
+        const int j = lt + k * P::TPF;
+        if (EXACT || j < NB)
+          sfor<R>([&](auto r_) {
+            constexpr int r = decltype(r_)::value;
+            pre[k][r] = __ldcs(gi + j + r * NB);
+          });
+      });
+    }
+  };
+  long long t = blockIdx.x;
+  fetch(t);
+  for (; t < ntiles; t += gridDim.x) {
+    const long long tr = t * P::FPB + f;
+    const bool fvalid = tr < batch;
+    float2 v[KB][R];
+    sfor<KB>([&](auto k_) {
+      constexpr int k = decltype(k_)::value;
+      sfor<R>([&](auto r_) {
+        constexpr int r = decltype(r_)::value;
+        v[k][r] = make_float2(pre[k][r].x, csign * pre[k][r].y);
+      });
+    });
+    fetch(t + gridDim.x);  // next tile's stage-0 inputs: in flight during this tile's stages
+    // stage 0 from registers (Ns = 1: no twiddle, outputs j R + r) into the exchange buffer
+    sfor<KB>([&](auto k_) {
+      constexpr int k = decltype(k_)::value;
+      const int j = lt + k * P::TPF;
+      if (fvalid && (EXACT || j < NB)) {
+        Codelet<R>::run(v[k]);
+        sfor<R>([&](auto r_) {
+          constexpr int r = decltype(r_)::value;
+          sm[P::sidx(f, j * R + r)] = v[k][r];
+        });
+      }
+    });
+    P::sync();
+    float2* go = out + tr * N;
+    sfor<P::S - 1>([&](auto s_) {
+      constexpr int s = decltype(s_)::value + 1;
+      stage<P, s, false, s == P::S - 1>(
+          sm, f, lt, fvalid, tw, [&](int, int) { return make_float2(0.f, 0.f); },
+          [&](int i, float2 w, int) { __stcs(go + i, make_float2(w.x, csign * w.y)); });
+    });
+    P::sync();  // the exchange buffer is free for the next tile's stage 0
+  }
+}
+
+template <class P, int MINB>
+static cudaError_t launch_fused_pipe(const float2* in, float2* out, const float2* tw, long long batch, int conj,
+                                     cudaStream_t st) {
+  auto kern = k_fused_pipe<P, MINB>;
+  static int grid_max = 0;
+  if (!grid_max) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::SMEM);
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, P::THREADS, P::SMEM);
+    if (e != cudaSuccess) return e;
+    grid_max = sms * (per > 0 ? per : 1);
+  }
+  const long long ntiles = (batch + P::FPB - 1) / P::FPB;
+  if (ntiles == 0) return cudaSuccess;
+  const unsigned grid = (unsigned)(ntiles < grid_max ? ntiles : grid_max);
+  kern<<<grid, P::THREADS, P::SMEM, st>>>(in, out, tw, batch, conj ? -1.0f : 1.0f);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- persistent TMA-fed kernel
 // LT_FAST schedules (S >= 2).  Each CTA loops over tiles of FPB contiguous transforms.
 // A tile is brought HBM -> shared by one bulk asynchronous copy (cp.async.bulk, TMA

@@ -19,6 +19,11 @@ namespace fftc {
   {N, RAD::S, {__VA_ARGS__}, TPF, FPB, TPF * FPB, 2, Sched<N, RAD, TPF, FPB, LT_FAST>::SMEM * 2,    \
    &launch_fused_tma<Sched<N, RAD, TPF, FPB, LT_FAST>, MINB>, NAME}
 
+// persistent, register-pipelined variant (LT_FAST direct schedules)
+#define FFTC_PIPE(NAME, N, RAD, TPF, FPB, MINB, ...)                                              \
+  {N, RAD::S, {__VA_ARGS__}, TPF, FPB, TPF * FPB, 3, Sched<N, RAD, TPF, FPB, LT_FAST>::SMEM,      \
+   &launch_fused_pipe<Sched<N, RAD, TPF, FPB, LT_FAST>, MINB>, NAME}
+
 using Rad_8 = Radices<8>;
 using Rad_16 = Radices<16>;
 using Rad_32 = Radices<32>;

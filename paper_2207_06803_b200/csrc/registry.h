@@ -14,7 +14,7 @@ struct FusedEntry {
   int S;
   int R[8];
   int tpf, fpb, threads;
-  int direct;  // 1: HBM I/O in the first/last stage (2: TMA bulk-copy fed, persistent); 0: staged through shared memory
+  int direct;  // 1: HBM I/O in the first/last stage (2: TMA bulk-copy fed, persistent; 3: register-pipelined, persistent); 0: staged through shared memory
   size_t smem;
   batch_launch_fn launch;
   const char* name;
