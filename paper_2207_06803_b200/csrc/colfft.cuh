@@ -120,12 +120,9 @@ static cudaError_t launch_colx(const float2* in, float2* out, const float2* tw, 
                                const float2* twB, const ColGeom& g, long long groups, int conj_in,
                                int conj_out, cudaStream_t st) {
   auto kern = k_colx<P, OUT_T, MINB>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::SMEM);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static const cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                       (int)P::SMEM);  // once, thread-safe
+  if (attr != cudaSuccess) return attr;
   const long long grid = groups * g.tiles;
   if (grid == 0) return cudaSuccess;
   if (grid > 0x7fffffffLL) return cudaErrorInvalidValue;

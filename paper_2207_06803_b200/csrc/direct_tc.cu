@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "direct_tc.h"
+#include "launch_util.h"
 #include "tma.cuh"
 
 namespace fftc {
@@ -252,17 +253,10 @@ cudaError_t launch_direct(const float2* in, float2* out, const float* g_img, lon
   constexpr size_t smem = (size_t)(S + 1) * kTileM * 2 * N * 4 + (size_t)2 * (2 * N) * (2 * N) * 4 + 1024;
   static_assert(PER_SM * smem <= 227 * 1024, "CTAs per SM must fit in shared memory");
   auto kern = k_direct_tc<N, S>;
-  static int grid_max = 0;
-  if (!grid_max) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess)  // let PER_SM CTAs share an SM
-      e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (e != cudaSuccess) return e;
-    int dev = 0, sms = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    grid_max = PER_SM * sms;
-  }
+  // carveout 100: let PER_SM CTAs share an SM
+  static const KernelSetup ks = kernel_setup(kern, 128, smem, 100, PER_SM);
+  if (ks.err != cudaSuccess) return ks.err;
+  const int grid_max = ks.grid_max;
   CUtensorMap ti, to;
   if (!map_rows(&ti, in, N, batch) || !map_rows(&to, out, N, batch)) return cudaErrorInvalidValue;
   const long long T = (batch + kTileM - 1) / kTileM;

@@ -58,12 +58,9 @@ template <class P, int MINB>
 cudaError_t launch_rows(const float2* work, float2* out, const float2* tw, int M, long long N, long long batch,
                         int conj, cudaStream_t st) {
   auto kern = k_rows<P, MINB>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::SMEM);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static const cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                       (int)P::SMEM);  // once, thread-safe
+  if (attr != cudaSuccess) return attr;
   const long long grid = batch * (M / P::FPB);
   if (grid == 0) return cudaSuccess;
   if (grid > 0x7fffffffLL) return cudaErrorInvalidValue;

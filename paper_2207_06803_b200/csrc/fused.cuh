@@ -24,6 +24,7 @@
 //            f*(N|1) + i (odd stride -> conflict free across transforms).
 #pragma once
 #include "codelets.cuh"
+#include "launch_util.h"
 #include "tma.cuh"
 
 namespace fftc {
@@ -377,12 +378,9 @@ template <class P, bool DIRECT, int MINB>
 static cudaError_t launch_fused_batch(const float2* in, float2* out, const float2* tw, long long batch,
                                       int conj, cudaStream_t st) {
   auto kern = k_fused_batch<P, DIRECT, MINB>;
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::SMEM);
-    if (e != cudaSuccess) return e;
-    attr_done = true;
-  }
+  static const cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                       (int)P::SMEM);  // once, thread-safe
+  if (attr != cudaSuccess) return attr;
   const long long grid = (batch + P::FPB - 1) / P::FPB;
   if (grid == 0) return cudaSuccess;
   if (grid > 0x7fffffffLL) return cudaErrorInvalidValue;
@@ -464,17 +462,9 @@ template <class P, int MINB>
 static cudaError_t launch_fused_pipe(const float2* in, float2* out, const float2* tw, long long batch, int conj,
                                      cudaStream_t st) {
   auto kern = k_fused_pipe<P, MINB>;
-  static int grid_max = 0;
-  if (!grid_max) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::SMEM);
-    if (e != cudaSuccess) return e;
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, P::THREADS, P::SMEM);
-    if (e != cudaSuccess) return e;
-    grid_max = sms * (per > 0 ? per : 1);
-  }
+  static const KernelSetup ks = kernel_setup(kern, P::THREADS, P::SMEM);
+  if (ks.err != cudaSuccess) return ks.err;
+  const int grid_max = ks.grid_max;
   const long long ntiles = (batch + P::FPB - 1) / P::FPB;
   if (ntiles == 0) return cudaSuccess;
   const unsigned grid = (unsigned)(ntiles < grid_max ? ntiles : grid_max);
@@ -558,17 +548,9 @@ static cudaError_t launch_fused_tma(const float2* in, float2* out, const float2*
                                     cudaStream_t st) {
   auto kern = k_fused_tma<P, MINB>;
   constexpr size_t smem = (size_t)((((P::SS * P::FPB) + 1) & ~1) + P::N * P::FPB) * sizeof(float2);
-  static int grid_max = 0;
-  if (!grid_max) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, P::THREADS, smem);
-    if (e != cudaSuccess) return e;
-    grid_max = sms * (per > 0 ? per : 1);
-  }
+  static const KernelSetup ks = kernel_setup(kern, P::THREADS, smem);
+  if (ks.err != cudaSuccess) return ks.err;
+  const int grid_max = ks.grid_max;
   const long long ntiles = (batch + P::FPB - 1) / P::FPB;
   if (ntiles == 0) return cudaSuccess;
   const unsigned grid = (unsigned)(ntiles < grid_max ? ntiles : grid_max);

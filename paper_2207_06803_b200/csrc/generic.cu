@@ -69,13 +69,9 @@ cudaError_t launch_generic(const GenericSched& g, const float2* in, float2* out,
   int fpb = (int)(2048 / g.N);
   if (fpb < 1) fpb = 1;
   const size_t smem = (size_t)2 * fpb * g.N * sizeof(float2);
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(k_generic, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(2 * kGenericMaxN * sizeof(float2)));
-    if (e != cudaSuccess) return e;
-    attr_done = true;
-  }
+  static const cudaError_t attr = cudaFuncSetAttribute(k_generic, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                       (int)(2 * kGenericMaxN * sizeof(float2)));  // once
+  if (attr != cudaSuccess) return attr;
   const long long grid = (batch + fpb - 1) / fpb;
   if (grid == 0) return cudaSuccess;
   if (grid > 0x7fffffffLL) return cudaErrorInvalidValue;

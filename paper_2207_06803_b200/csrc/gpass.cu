@@ -163,13 +163,9 @@ int gpass_split(long long N, int* Ls, int max, int max_prime, int max_len) {
 
 cudaError_t gpass_execute(const GPassPlanData& d, const float2* in, float2* out, float2* work, long long batch,
                           int conj, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_gpass, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(2 * 256 * 17 * sizeof(float2)));  // max over L of 2 cols (L+1)
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static const cudaError_t attr = cudaFuncSetAttribute(k_gpass, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                       (int)(2 * 256 * 17 * sizeof(float2)));  // max over L
+  if (attr != cudaSuccess) return attr;
   const float2* src = in;
   for (int s = 0; s < d.p; ++s) {
     float2* dst = ((d.p - 1 - s) % 2 == 0) ? out : work;  // the last pass lands in out

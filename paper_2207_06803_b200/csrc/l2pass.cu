@@ -22,6 +22,7 @@
 #include <string.h>
 
 #include "l2pass.h"
+#include "launch_util.h"
 #include "passtile.cuh"
 
 namespace fftc {
@@ -254,17 +255,9 @@ template <class PA, class PB, int MINB>
 cudaError_t launch_l2(const L2Params& q, cudaStream_t st) {
   constexpr size_t smem = (size_t)kStages * PA::N * 16 * sizeof(float2) + 1024;
   auto kern = k_l2<PA, PB, MINB>;
-  static int grid_max = 0;
-  if (!grid_max) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kThreads, smem);
-    if (e != cudaSuccess) return e;
-    grid_max = sms * (per > 0 ? per : 1);
-  }
+  static const KernelSetup ks = kernel_setup(kern, kThreads, smem);
+  if (ks.err != cudaSuccess) return ks.err;
+  const int grid_max = ks.grid_max;
   const char* g = getenv("FFTC_L2_GRID");  // tuning
   int grid = g ? atoi(g) : grid_max;
   if (grid > grid_max || grid < 1) grid = grid_max;

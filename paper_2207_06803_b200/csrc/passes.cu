@@ -20,6 +20,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include "launch_util.h"
 #include "passes.h"
 #include "passtile.cuh"
 #include "tma.cuh"
@@ -106,19 +107,12 @@ cudaError_t launch_pass(bool first, const CUtensorMap& tin, const CUtensorMap& t
                         const float2* tw, const float2* twA, const float2* twB, const PassGeom& g, int conj_in,
                         int conj_out, cudaStream_t st) {
   constexpr size_t smem = (size_t)NBUF * P::N * P::FPB * sizeof(float2) + 1024;
-  static int grid_max[2] = {0, 0};
   auto kern = first ? k_pass<P, true, MINB, NBUF> : k_pass<P, false, MINB, NBUF>;
-  int& gm = grid_max[first ? 1 : 0];
-  if (!gm) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, P::THREADS, smem);
-    if (e != cudaSuccess) return e;
-    gm = sms * (per > 0 ? per : 1);
-  }
+  static const KernelSetup ks_first = kernel_setup(k_pass<P, true, MINB, NBUF>, P::THREADS, smem);
+  static const KernelSetup ks_later = kernel_setup(k_pass<P, false, MINB, NBUF>, P::THREADS, smem);
+  const KernelSetup& ks = first ? ks_first : ks_later;
+  if (ks.err != cudaSuccess) return ks.err;
+  const int gm = ks.grid_max;
   if (g.tiles_total == 0) return cudaSuccess;
   const unsigned grid = (unsigned)(g.tiles_total < gm ? g.tiles_total : gm);
   kern<<<grid, P::THREADS, smem, st>>>(tin, tout, out_first, tw, twA, twB, g, conj_in ? -1.f : 1.f,

@@ -52,3 +52,39 @@ def test_graph_capture_l2_resident(monkeypatch):
     """The L2-resident kernel (cooperative launch + counter reset) inside a captured graph."""
     monkeypatch.setenv("FFTC_LARGE", "l2")
     test_graph_capture_replays_eager_result("l2", lambda: fftc.Plan(1 << 16, 37, -1), 1 << 16, 37)
+
+
+def test_concurrent_plans_from_host_threads():
+    """Plans of every kind created and executed concurrently from 6 host threads, each on its
+    own stream (first-use kernel setup and the JIT cache are thread-safe); results equal the
+    single-threaded ones bit for bit."""
+    import threading
+    kinds = [(64, 999, -1), (3125, 21, 1), (48, 77, -1), (1 << 16, 3, -1), (143, 40, 1), (100000, 2, -1)]
+    xs = {k: torch.from_numpy(synth.uniform_c64(k[0], k[1], seed=k[0]).reshape(-1)).cuda() for k in kinds}
+    ref = {}
+    for k in kinds:
+        with fftc.Plan(*k) as p:
+            ref[k] = p(xs[k]).cpu().numpy()
+    out, errors = {}, []
+
+    def work(k):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for _ in range(3):
+                    with fftc.Plan(*k) as p:
+                        y = torch.empty_like(xs[k])
+                        p.execute(xs[k], y, stream=s.cuda_stream)
+                s.synchronize()
+                out[k] = y.cpu().numpy()
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append((k, e))
+
+    ts = [threading.Thread(target=work, args=(k,)) for k in kinds]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
+    for k in kinds:
+        assert np.array_equal(out[k].view(np.uint32), ref[k].view(np.uint32)), k

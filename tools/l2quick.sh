@@ -1,3 +1,2 @@
 cd $GRAFT_REPO_ROOT
-timeout 600 python -m pytest tests/test_gpu_parity.py -q -m gpu -p no:cacheprovider --timeout 300 -x -k "candidate" 2>&1 | tail -1
-python tools/tune.py 4096 2048
+timeout 900 python -m pytest tests/test_gpu_graph.py tests/test_direct_tc.py tests/test_gpu_parity.py -q -m gpu -p no:cacheprovider --timeout 300 -x -k "graph or concurrent or direct or small_batches or config1 or multipass or candidate" 2>&1 | tail -3
