@@ -159,12 +159,21 @@ static const PassEntry kPasses[] = {
     FFTC_PASS8("p512_r16x32_c8t32m1", 512, PRad_16x32, 32, 1, 2, 16, 32),
     FFTC_PASS8("p1024_r32x32_c8b2", 1024, PRad_32x32, 32, 1, 2, 32, 32),
     FFTC_PASS8("p1024_r32x32_c8b1", 1024, PRad_32x32, 32, 3, 1, 32, 32),
+    FFTC_PASS8("p1024_r32x32_c8b1m2", 1024, PRad_32x32, 32, 2, 1, 32, 32),
+    FFTC_PASS8("p1024_r16x64t16_c8b1m2", 1024, PRad_32x32, 16, 2, 1, 32, 32),
 };
 
-const PassEntry* find_pass(int L) {
+const PassEntry* find_pass(int L, long long N) {
   if (const char* want = getenv("FFTC_PASS"))
     for (const auto& e : kPasses)
       if (e.L == L && strcmp(e.name, want) == 0) return &e;
+  // measured on B200 (profiles/r01h): in the two-pass 2^20 plan the 1024-long pass runs
+  // fastest as one 64 KB buffer x 2 CTAs/SM (1.57 vs 1.70 ms); in the three-pass 2^27/2^28
+  // plans the double-buffered single CTA wins (2.66 vs 2.75 ms)
+  const char* pick = (L == 1024 && N > 0 && N <= (1LL << 20)) ? "p1024_r32x32_c8b1m2" : nullptr;
+  if (pick)
+    for (const auto& e : kPasses)
+      if (e.L == L && strcmp(e.name, pick) == 0) return &e;
   for (const auto& e : kPasses)
     if (e.L == L) return &e;
   return nullptr;

@@ -40,7 +40,9 @@ struct PassPlanData {
   int tws[kMaxPasses] = {};      // split of the pass twiddle tables (balanced: ceil(log2(Ns L) / 2))
 };
 
-const PassEntry* find_pass(int L);
+// Compiled pass kernel for length L (default per L, or a measured choice for the plan's N;
+// FFTC_PASS=<name> overrides).
+const PassEntry* find_pass(int L, long long N = 0);
 bool passes_available();
 int pass_split(long long N, int* Ls, int max);
 cudaError_t passes_execute(const PassPlanData& pp, const float2* in, float2* out, float2* work, long long batch,
