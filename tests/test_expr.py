@@ -146,3 +146,33 @@ def test_gpu_expr(radices):
             p.close()
         err = oracle.rel_l2(y, oracle.fft_ct(x, sign)).max()
         assert err <= min(oracle.tolerance(N), 2e-6), (radices, sign, err, d)
+
+
+# ---------------------------------------------------------------- property tests (hypothesis)
+from hypothesis import given, settings, strategies as st  # noqa: E402
+
+
+@settings(max_examples=200, deadline=None)
+@given(st.lists(st.sampled_from([2, 3, 4, 5, 7, 8, 9, 16]), min_size=1, max_size=5), st.booleans())
+def test_any_recursive_eq2_expression_round_trips(radices, ascii_ops):
+    """Any right-recursive Eq. 2 expression parses back to its radix list (a lone DFT(n) is
+    left to the planner)."""
+    s, _ = eq2_expr(radices, ascii_ops=ascii_ops, with_matrix=False)
+    want = radices if len(radices) > 1 else []
+    assert fftc.fftc_expr_radices(s) == (math.prod(radices), want)
+
+
+@settings(max_examples=300, deadline=None)
+@given(st.lists(st.sampled_from([2, 3, 4, 5]), min_size=2, max_size=3), st.integers(0, 10 ** 6), st.integers(0, 4))
+def test_mutated_expressions_fail_cleanly(radices, pos, kind):
+    """Mutations of a valid expression (a dropped / swapped / altered character) either still
+    parse to some valid schedule or raise ValueError -- never crash or hang the parser."""
+    s, _ = eq2_expr(radices, with_matrix=False)
+    i = pos % len(s)
+    mut = [s[:i] + s[i + 1:], s[:i] + "(" + s[i:], s[:i] + ")" + s[i:], s[:i] + "9" + s[i + 1:],
+           s.replace("I(", "DFT(", 1)][kind]
+    try:
+        N, R = fftc.fftc_expr_radices(mut)
+        assert N >= 1 and (not R or math.prod(R) == N)
+    except ValueError:
+        pass
