@@ -112,6 +112,30 @@ def test_every_pass_candidate(n, name, monkeypatch):
         check(gpu_fft(x, sign), x, sign)
 
 
+# ---------------------------------------------------------------- random large sizes
+def _random_large_sizes(count=24, seed=2207):
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < count:
+        e = rng.integers(0, [23, 12, 8, 6])  # 2^a 3^b 5^c 7^d
+        n = 2 ** int(e[0]) * 3 ** int(e[1]) * 5 ** int(e[2]) * 7 ** int(e[3])
+        if 4096 < n <= (1 << 22):
+            out.append(n)
+    return sorted(set(out))
+
+
+@pytest.mark.parametrize("N", _random_large_sizes())
+def test_random_large_sizes(N):
+    """Seeded random 7-smooth N in (4096, 2^22]: whichever large-N path the planner picks
+    (TMA passes or runtime passes), ragged batch, both signs, against the oracle."""
+    batch = max(1, (1 << 21) // N) | 1
+    x = synth.uniform_c64(N, batch, seed=N % 1009)
+    idx = np.array(sorted({0, batch // 2, batch - 1}))
+    for sign in (-1, 1):
+        y = gpu_fft(x, sign)
+        check(y[idx], x[idx], sign)
+
+
 # ---------------------------------------------------------------- beyond 2^31 elements
 @pytest.mark.parametrize("N,batch", [(64, (1 << 25) + 3), (4096, (1 << 19) + 5), (1 << 16, (1 << 15) + 1)])
 def test_more_than_2p31_elements(N, batch):
