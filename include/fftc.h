@@ -221,6 +221,7 @@ fftc_plan* fftc_dist_plan_create(int64_t N, int sign, const void* nccl_id, int r
  * FFTC_DIST_PEER_STORES: fuse the exchanges into the kernels around them:
  *   the pack kernel stores each chunk straight into the receiving rank's
  *   buffer and the DFT_M kernel's epilogue does the same for exchange #2
+ *   (and the DFT_K epilogue for exchange #3 when DFT_K is one pass)
  *   (P2P stores over NVLink into buffers mapped by CUDA IPC, handles
  *   all-gathered over NCCL at create; a 1-int NCCL all-reduce orders each
  *   exchange).  nranks <= 8.                                               */

@@ -231,6 +231,7 @@ fftc_status dist_execute(DistState* d, const void* in, void* out, cudaStream_t s
   const int64_t chunk = Mp * Kp;
   float2* recvA = d->recv;                 // exchange #1 lands here
   float2* recvB = peer ? d->recv2 : d->recv;  // exchange #2 lands here
+  const bool fuse3 = peer && !tout && d->K2 == 1;  // exchange #3 fused into the DFT_K epilogue
   if (peer) {
     // 1+2. pack fused with exchange #1: x_p[ql][d][rl] -> rank d's recvA[p][ql][rl] (NVLink stores)
     e = barrier(d, st, &ns);  // every rank is done reading its receive buffers (previous call)
@@ -284,6 +285,14 @@ fftc_status dist_execute(DistState* d, const void* in, void* out, cudaStream_t s
       g.out_c = 1;
       g.out_s = Mp;
       g.ocl = 62;
+      if (fuse3) {
+        // exchange #3 fused: output k1 goes to rank k1 / Kp's recvA[p][k1 mod Kp][jl] (recvA is
+        // free: every rank passed the barrier after its DFT_M, the last reader of recvA)
+        const int prank = d->loopback ? p : d->rank;
+        g.ocl = ilog2ll(Kp);
+        g.npeer = (int)P;
+        for (int q = 0; q < P; ++q) g.peer[q] = (unsigned long long)(d->peerA[q] + prank * chunk);
+      }
       e = d->cK1->launch(recvB + p * slab, kout, d->twK1, nullptr, nullptr, g, 1, 0, cj, st);
     } else {
       const int64_t K1 = d->K1, K2 = d->K2;
@@ -310,8 +319,8 @@ fftc_status dist_execute(DistState* d, const void* in, void* out, cudaStream_t s
     }
   }
   if (!tout) {
-    // 6. a2a #3
-    if (e == cudaSuccess) e = all_to_all(d, st, &ns);
+    // 6. a2a #3 (fused: the barrier after the peer stores)
+    if (e == cudaSuccess) e = fuse3 ? barrier(d, st, &ns) : all_to_all(d, st, &ns);
     // 7. unpack: recv viewed as [s][k1l][jl] (P, Kp, Mp) -> X_p[k1l M + s Mp + jl]
     for (int p = 0; p < d->nloc && e == cudaSuccess; ++p)
       e = permute3(d->recv + p * slab, X + p * slab, P, Kp, Mp, Mp, M, conj, st);
@@ -355,7 +364,10 @@ int dist_describe(const DistState* d, char* buf, size_t len) {
                   (long long)d->N, d->P, d->rank, d->sign, (long long)d->M, (long long)d->K, (long long)d->K1,
                   (long long)d->K2, (long long)d->Mp, (long long)d->Kp, (int)d->loopback, d->launches,
                   (d->flags & FFTC_DIST_TRANSPOSED_OUT) ? 2 : 3,
-                  (d->flags & FFTC_DIST_PEER_STORES) ? "peer-stores(#1,#2 fused)" : "nccl",
+                  (d->flags & FFTC_DIST_PEER_STORES)
+                      ? (((d->flags & FFTC_DIST_TRANSPOSED_OUT) || d->K2 != 1) ? "peer-stores(#1,#2 fused)"
+                                                                                : "peer-stores(#1,#2,#3 fused)")
+                      : "nccl",
                   (d->flags & FFTC_DIST_TRANSPOSED_OUT) ? "transposed" : "natural",
                   (long long)(d->Mp * d->Kp * (int64_t)sizeof(float2)));
 }
