@@ -46,6 +46,7 @@ struct Parser {
   const char* s;
   size_t i = 0;
   std::string err;
+  int depth = 0;  // parenthesis nesting (bounded: the recursion stays on a small stack)
 
   void ws() {
     while (s[i] && isspace((unsigned char)s[i])) ++i;
@@ -119,8 +120,13 @@ struct Parser {
   std::unique_ptr<Node> factor() {
     ws();
     if (s[i] == '(') {
+      if (++depth > 64) {
+        fail("nesting deeper than 64");
+        return nullptr;
+      }
       ++i;
       auto e = expr();
+      --depth;
       if (!e || !expect(')')) return nullptr;
       return e;
     }

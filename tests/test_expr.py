@@ -97,6 +97,7 @@ BAD = [
     "DFT(4) extra",
     "",
     "InputComplex",
+    "(" * 100000 + "DFT(4)" + ")" * 100000,   # pathological nesting: rejected, no stack overflow
 ]
 
 
