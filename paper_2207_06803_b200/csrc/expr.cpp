@@ -160,7 +160,12 @@ struct Parser {
   std::unique_ptr<Node> term() {
     auto l = factor();
     if (!l) return nullptr;
+    int nk = 0;
     while (kron_op()) {
+      if (++nk > 64) {
+        fail("more than 64 Kronecker factors");
+        return nullptr;
+      }
       auto r = factor();
       if (!r) return nullptr;
       auto k = std::make_unique<Node>();
@@ -180,6 +185,10 @@ struct Parser {
     m->k = N_MUL;
     m->kids.push_back(std::move(l));
     do {
+      if (m->kids.size() > 256) {
+        fail("more than 256 product factors");
+        return nullptr;
+      }
       auto r = term();
       if (!r) return nullptr;
       m->kids.push_back(std::move(r));

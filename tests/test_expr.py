@@ -98,6 +98,8 @@ BAD = [
     "",
     "InputComplex",
     "(" * 100000 + "DFT(4)" + ")" * 100000,   # pathological nesting: rejected, no stack overflow
+    "DFT(2)" + " ⊗ I(1)" * 100000,             # pathological Kronecker chain
+    " · ".join(["I(2)"] * 100000),              # pathological product chain
 ]
 
 
