@@ -112,6 +112,19 @@ def test_every_pass_candidate(n, name, monkeypatch):
         check(gpu_fft(x, sign), x, sign)
 
 
+# ---------------------------------------------------------------- the paper's own check
+def test_paper_protocol_p217_on_gpu():
+    """The paper's accuracy experiment on the GPU path: random inputs, N = 32..1024,
+    ten runs each, max |result - reference| / N < 1e-7 -- with the fp64 oracle as the
+    reference (the paper compared against numpy) and the fp32 GPU result."""
+    for N in [32, 64, 128, 256, 512, 1024]:
+        x = synth.uniform_c64(N, 10, seed=1000 * N)
+        for sign in (-1,):
+            y = gpu_fft(x, sign).astype(np.complex128)
+            ref = oracle.fft_ct(x, sign)
+            assert (np.abs(y - ref).max(axis=1) / N < 1e-7).all(), N
+
+
 # ---------------------------------------------------------------- random large sizes
 def _random_large_sizes(count=24, seed=2207):
     rng = np.random.default_rng(seed)
