@@ -68,12 +68,15 @@ __global__ void __launch_bounds__(P::THREADS, MINB)
     float2* sm = buf0 + k * L * C;
     const int b = (int)(t / tpb), c0 = (int)(t % tpb) * C;
     const int c = c0 + f;
+    PassTwPre pre{};
+    if constexpr (!FIRST) pre = pass_tw_pre<P>(c, lt, g.Ns, twA, twB, g.tws);  // under the TMA wait
     mbar_wait(&full[k], NBUF == 2 ? ((it >> 1) & 1) : (it & 1));
     // first pass, 8-column tiles: one TMA store of the tile in the pass-0 output layout
     // (measured faster for L = 512/1024); 16-column tiles: coalesced 8-byte stores, lanes
     // walking each column's contiguous outputs (measured faster for L <= 256)
     constexpr bool TMA0 = FIRST && C == 8;
-    pass_tile<P, !FIRST, TMA0>(sm, f, lt, c, g.Ns, tw, twA, twB, g.tws, csign_in, csign_out);
+    pass_tile<P, !FIRST, TMA0>(sm, f, lt, c, g.Ns, tw, twA, twB, g.tws, csign_in, csign_out,
+                               FIRST ? nullptr : &pre);
     if constexpr (FIRST && !TMA0) {
       __syncthreads();
       pass0_store<P>(sm, out_first + (long long)b * g.N + (long long)c0 * L,
@@ -160,7 +163,6 @@ static const PassEntry kPasses[] = {
     FFTC_PASS8("p1024_r32x32_c8b2", 1024, PRad_32x32, 32, 1, 2, 32, 32),
     FFTC_PASS8("p1024_r32x32_c8b1", 1024, PRad_32x32, 32, 3, 1, 32, 32),
     FFTC_PASS8("p1024_r32x32_c8b1m2", 1024, PRad_32x32, 32, 2, 1, 32, 32),
-    FFTC_PASS8("p1024_r16x64t16_c8b1m2", 1024, PRad_32x32, 16, 2, 1, 32, 32),
 };
 
 const PassEntry* find_pass(int L, long long N) {

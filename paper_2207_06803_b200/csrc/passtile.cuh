@@ -28,11 +28,38 @@ __device__ __forceinline__ int out0_idx(int f, int k) {
   return (((k >> 4) * P::FPB + f) << 4) + ((((k & 15) >> 1) ^ (f & 7)) << 1) + (k & 1);
 }
 
+// The input twiddles of one thread's sub-stage-0 butterfly (every pass kernel has one per
+// thread: NB0 <= TPF): w^{m j} and the step powers w^{m NB0 2^b}.  They depend only on the
+// column and the lane, so the kernels compute them before waiting for the tile's TMA load and
+// the table latency hides under it.
+struct PassTwPre {
+  float2 sp[5];
+  float2 base;
+};
+template <class P>
+__device__ __forceinline__ PassTwPre pass_tw_pre(int c, int lt, int Ns, const float2* __restrict__ twA,
+                                                 const float2* __restrict__ twB, int tws) {
+  constexpr int L = P::N;
+  constexpr int R0 = P::R(0);
+  constexpr int NB0 = L / R0;
+  constexpr int NB2 = ilog2(highbit(R0 - 1)) + 1;
+  static_assert(NB2 <= 5 && NB0 <= P::TPF, "one sub-stage-0 butterfly per thread");
+  PassTwPre t;
+  const long long m = (long long)(c % Ns);
+  t.sp[0] = root_lookup_s(twA, twB, m * NB0, tws);
+  sfor<NB2 - 1>([&](auto b_) {
+    constexpr int bb = decltype(b_)::value + 1;
+    t.sp[bb] = cmul(t.sp[bb - 1], t.sp[bb - 1]);
+  });
+  t.base = lt < NB0 ? root_lookup_s(twA, twB, m * lt, tws) : make_float2(1.f, 0.f);
+  return t;
+}
+
 template <class P, bool TW, bool OUT0 = false>
 __device__ __forceinline__ void pass_tile(float2* sm, int f, int lt, int c, int Ns,
                                           const float2* __restrict__ tw, const float2* __restrict__ twA,
                                           const float2* __restrict__ twB, int tws, float csign_in,
-                                          float csign_out) {
+                                          float csign_out, const PassTwPre* pre = nullptr) {
   static_assert((P::FPB == 16 && P::LAY == LAY_TMA128) || (P::FPB == 8 && P::LAY == LAY_TMA64),
                 "pass tiles: 16 columns with the TMA 128B swizzle or 8 columns with the 64B swizzle");
   constexpr int L = P::N;
@@ -43,18 +70,25 @@ __device__ __forceinline__ void pass_tile(float2* sm, int f, int lt, int c, int 
   const long long m = TW ? (long long)(c % Ns) : 0;
   float2 sp[NB2];
   if constexpr (TW) {
-    sp[0] = root_lookup_s(twA, twB, m * NB0, tws);
-    sfor<NB2 - 1>([&](auto b_) {
-      constexpr int bb = decltype(b_)::value + 1;
-      sp[bb] = cmul(sp[bb - 1], sp[bb - 1]);
-    });
+    if (pre) {
+      sfor<NB2>([&](auto b_) {
+        constexpr int bb = decltype(b_)::value;
+        sp[bb] = pre->sp[bb];
+      });
+    } else {
+      sp[0] = root_lookup_s(twA, twB, m * NB0, tws);
+      sfor<NB2 - 1>([&](auto b_) {
+        constexpr int bb = decltype(b_)::value + 1;
+        sp[bb] = cmul(sp[bb - 1], sp[bb - 1]);
+      });
+    }
   }
   float2 base = make_float2(1.f, 0.f);
   auto gload = [&](int i, int r) {
     float2 v = sm[P::sidx(f, i)];
     v.y *= csign_in;
     if constexpr (TW) {
-      if (r == 0) base = root_lookup_s(twA, twB, m * i, tws);
+      if (r == 0) base = pre ? pre->base : root_lookup_s(twA, twB, m * i, tws);
       float2 w = base;
       sfor<NB2>([&](auto b_) {
         constexpr int bb = decltype(b_)::value;
