@@ -18,7 +18,8 @@ import ctypes
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libfftc.so")
+# FFTC_LIB_PATH: an alternative in-tree build of the same library (A/B timing of build variants).
+LIB_PATH = os.environ.get("FFTC_LIB_PATH") or os.path.join(_PKG, "libfftc.so")
 
 FFTC_SUCCESS = 0
 FFTC_ERROR_INVALID_VALUE = 1

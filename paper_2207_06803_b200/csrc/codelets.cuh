@@ -188,12 +188,54 @@ struct Codelet<P, std::enable_if_t<(P > 2) && is_prime(P)>> {
   }
 };
 
-// Composite R = M*K: Eq. 2 in registers.
+constexpr int gcd_c(int a, int b) { return b == 0 ? a : gcd_c(b, a % b); }
+// a^-1 mod m for gcd(a, m) == 1 (brute force: m is a codelet factor).
+constexpr int inv_mod(int a, int m) {
+  for (int x = 1; x < m; ++x)
+    if ((a * x) % m == 1) return x;
+  return m == 1 ? 0 : -1;
+}
+
+// Composite R = M*K: Eq. 2 in registers.  When gcd(K, M) = 1 the twiddle D^R_M is
+// folded into index maps instead (Good-Thomas prime-factor form of the same DFT, DESIGN
+// reading 19): input n = (n1 M + n2 K) mod R, output k = CRT(k mod K, k mod M), so
+// w_R^{nk} = w_K^{n1 k1} w_M^{n2 k2} and no internal twiddle multiplies remain.
 template <int R>
 struct Codelet<R, std::enable_if_t<(R > 4) && !is_prime(R)>> {
   static constexpr int K = codelet_outer(R);
   static constexpr int M = R / K;
+  static constexpr bool kPfa = gcd_c(K, M) == 1;
   FFTC_HD static void run(float2* v) {
+    if constexpr (kPfa) run_pfa(v);
+    else run_ct(v);
+  }
+  FFTC_HD static void run_pfa(float2* v) {
+    constexpr int eK = M * inv_mod(M % K, K);  // = 1 mod K, 0 mod M
+    constexpr int eM = K * inv_mod(K % M, M);  // = 0 mod K, 1 mod M
+    float2 u[K][M];
+    sfor<K>([&](auto a_) {
+      constexpr int n1 = decltype(a_)::value;
+      sfor<M>([&](auto b_) {
+        constexpr int n2 = decltype(b_)::value;
+        u[n1][n2] = v[(n1 * M + n2 * K) % R];
+      });
+      Codelet<M>::run(u[n1]);
+    });
+    sfor<M>([&](auto b_) {
+      constexpr int k2 = decltype(b_)::value;
+      float2 w[K];
+      sfor<K>([&](auto a_) {
+        constexpr int n1 = decltype(a_)::value;
+        w[n1] = u[n1][k2];
+      });
+      Codelet<K>::run(w);
+      sfor<K>([&](auto a_) {
+        constexpr int k1 = decltype(a_)::value;
+        v[(k1 * eK + k2 * eM) % R] = w[k1];
+      });
+    });
+  }
+  FFTC_HD static void run_ct(float2* v) {
     float2 u[K][M];
     // Pi^R_K then I_K (x) DFT_M:  u_r[q] = x[q K + r]
     sfor<K>([&](auto r_) {

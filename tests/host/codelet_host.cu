@@ -1,6 +1,6 @@
 // Host-compiled check of the register codelets (codelets.cuh is __host__ __device__).
 // Prints, for each radix, y = DFT_R(x) for x[n] = (sin(n+1), cos(2n+1)) as "R k re im" lines;
-// tests/test_host_logic.py compares them with the oracle.
+// tests/test_codelets_host.py compares them with the oracle.
 #include <cmath>
 #include <cstdio>
 #include "../../paper_2207_06803_b200/csrc/codelets.cuh"
