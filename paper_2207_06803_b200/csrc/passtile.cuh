@@ -119,7 +119,9 @@ __device__ __forceinline__ void pass0_store(const float2* sm, float2* __restrict
     // columns 2q and 2q+1 of row r share one 16-byte chunk (q ^ (r & 7)) of the swizzled row:
     // one conflict-free 128-bit shared load per pair, two coalesced stores (lanes walk r).
     // Measured (same box A/B): 2^13 1.56 -> 1.52 ms; slower for L = 256 (2^16 1.50 -> 1.54 ms),
-    // which keeps the one-column-per-instruction walk below.
+    // which keeps the one-column-per-instruction walk below.  Its shared reads are 2-way
+    // conflicted (lanes repeat r & 7); a conflict-free walk (a warp = 16 rows x 2 columns,
+    // two full 128-byte lines per store) measured slower still: 2^16 1.49 -> 1.52 ms.
     constexpr int PER = L * (C / 2) / P::THREADS;
     static_assert((L * (C / 2)) % P::THREADS == 0, "tile must split evenly");
     sfor<PER>([&](auto n_) {
