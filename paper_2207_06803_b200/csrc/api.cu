@@ -345,7 +345,7 @@ fftc_plan* fftc_plan_create(int64_t N, int64_t batch, int sign) {
     p->pp.p = np;
     int64_t Ns = 1;
     for (int s = 0; s < np && err == cudaSuccess; ++s) {
-      const PassEntry* e = find_pass(Ls[s], N);
+      const PassEntry* e = find_pass(Ls[s], N, s == 0);
       if (!e) return fail(p, FFTC_ERROR_UNSUPPORTED_SIZE);
       p->pp.e[s] = e;
       const int64_t T = Ns * Ls[s];

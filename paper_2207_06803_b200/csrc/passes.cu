@@ -14,8 +14,11 @@
 // transformed in place, and -- for s > 0 -- written back by ONE 4-D TMA tensor store
 // (the autosort write is a [L][C] box of a
 // (Ns, L, NB/Ns, batch) view).  Pass 0 (Ns = 1) writes each column's L outputs
-// contiguously, via coalesced 8-byte stores.  CTAs are persistent and double-buffered:
-// the tile after next streams in while the current one is computed.
+// contiguously, via coalesced 8-byte stores.  CTAs are persistent with NBUF tile buffers:
+// NBUF <= 2 refills a buffer right after its store has read it (the tile after next streams
+// in while the current one is computed); NBUF >= 3 keeps NBUF - 1 loads ahead and refills the
+// buffer of the PREVIOUS tile at the end of each iteration, so the issuing thread never
+// waits on the store it has just committed.
 #include <cuda.h>
 #include <stdlib.h>
 #include <string.h>
@@ -34,12 +37,14 @@ __global__ void __launch_bounds__(P::THREADS, MINB)
     k_pass(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout,
            float2* __restrict__ out_first, const float2* __restrict__ tw, const float2* __restrict__ twA,
            const float2* __restrict__ twB, PassGeom g, float csign_in, float csign_out) {
-  static_assert(NBUF == 1 || NBUF == 2, "one or two tile buffers");
+  static_assert(NBUF >= 1 && NBUF <= 4, "one to four tile buffers");
+  constexpr bool RING = NBUF >= 3;            // deferred refill (see the file header)
+  constexpr int AHEAD = RING ? NBUF - 1 : NBUF;  // tiles issued before the first compute
   constexpr int L = P::N, C = P::FPB;
   constexpr uint32_t TILE_BYTES = (uint32_t)L * C * 8u;
   extern __shared__ __align__(1024) unsigned char smraw[];
   float2* buf0 = reinterpret_cast<float2*>(smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u));
-  __shared__ __align__(8) uint64_t full[2];
+  __shared__ __align__(8) uint64_t full[NBUF];
   int f, lt;
   P::thread_coords(threadIdx.x, f, lt);
   const long long T = g.tiles_total;
@@ -53,24 +58,21 @@ __global__ void __launch_bounds__(P::THREADS, MINB)
       tma_load_3d(buf0 + k * L * C + h * BOX * C, &tin, c0, h * BOX, b, &full[k]);
     });
   };
-  if (threadIdx.x == 0) {
-    mbar_init(&full[0], 1);
-    mbar_init(&full[1], 1);
-  }
+  if (threadIdx.x == 0)
+    for (int k = 0; k < NBUF; ++k) mbar_init(&full[k], 1);
   __syncthreads();
-  if (threadIdx.x == 0) {
-    if (blockIdx.x < T) issue(blockIdx.x, 0);
-    if (NBUF == 2 && blockIdx.x + gridDim.x < T) issue(blockIdx.x + gridDim.x, 1);
-  }
+  if (threadIdx.x == 0)
+    for (int k = 0; k < AHEAD; ++k)
+      if (blockIdx.x + (long long)k * gridDim.x < T) issue(blockIdx.x + (long long)k * gridDim.x, k);
   int it = 0;
   for (long long t = blockIdx.x; t < T; t += gridDim.x, ++it) {
-    const int k = NBUF == 2 ? (it & 1) : 0;
+    const int k = it % NBUF;
     float2* sm = buf0 + k * L * C;
     const int b = (int)(t / tpb), c0 = (int)(t % tpb) * C;
     const int c = c0 + f;
     PassTwPre pre{};
     if constexpr (!FIRST) pre = pass_tw_pre<P>(c, lt, g.Ns, twA, twB, g.tws);  // under the TMA wait
-    mbar_wait(&full[k], NBUF == 2 ? ((it >> 1) & 1) : (it & 1));
+    mbar_wait(&full[k], (it / NBUF) & 1);
     // first pass, 8-column tiles: one TMA store of the tile in the pass-0 output layout
     // (measured faster for L = 512/1024); 16-column tiles: coalesced 8-byte stores, lanes
     // walking each column's contiguous outputs (measured faster for L <= 256)
@@ -97,7 +99,14 @@ __global__ void __launch_bounds__(P::THREADS, MINB)
       }
       bulk_commit();
     }
-    if (threadIdx.x == 0 && t + NBUF * (long long)gridDim.x < T) {
+    if constexpr (RING) {
+      // refill the previous tile's buffer: its store (committed one iteration ago) has had a
+      // whole tile of compute to read it; the store just committed may stay in flight
+      if (threadIdx.x == 0 && t + AHEAD * (long long)gridDim.x < T) {
+        bulk_wait_read1();
+        issue(t + AHEAD * (long long)gridDim.x, (it + AHEAD) % NBUF);
+      }
+    } else if (threadIdx.x == 0 && t + NBUF * (long long)gridDim.x < T) {
       bulk_wait_read0();  // the store has finished reading this buffer
       issue(t + NBUF * (long long)gridDim.x, k);
     }
@@ -156,26 +165,52 @@ static const PassEntry kPasses[] = {
     FFTC_PASS("p256_r16x16", 256, PRad_16x16, 16, 3, 2, 16, 16),
     FFTC_PASS("p256_r16x16_b2m1", 256, PRad_16x16, 16, 1, 2, 16, 16),
     FFTC_PASS("p256_r16x16_b1m4", 256, PRad_16x16, 16, 4, 1, 16, 16),
+    FFTC_PASS("p256_r16x16_b3m2", 256, PRad_16x16, 16, 2, 3, 16, 16),
+    FFTC_PASS("p128_r16x8_b3m4", 128, PRad_16x8, 16, 4, 3, 16, 8),
+    FFTC_PASS("p128_r16x8_b4m3", 128, PRad_16x8, 16, 3, 4, 16, 8),
     FFTC_PASS8("p512_r16x32_c8t32", 512, PRad_16x32, 32, 2, 2, 16, 32),
     FFTC_PASS8("p512_r32x16_c8", 512, PRad_32x16, 16, 3, 2, 32, 16),
     FFTC_PASS8("p512_r32x16_c8m2", 512, PRad_32x16, 16, 2, 2, 32, 16),
     FFTC_PASS8("p512_r16x32_c8t32m1", 512, PRad_16x32, 32, 1, 2, 16, 32),
+    FFTC_PASS8("p512_r16x32_c8t32b3", 512, PRad_16x32, 32, 2, 3, 16, 32),
     FFTC_PASS8("p1024_r32x32_c8b2", 1024, PRad_32x32, 32, 1, 2, 32, 32),
     FFTC_PASS8("p1024_r32x32_c8b1", 1024, PRad_32x32, 32, 3, 1, 32, 32),
     FFTC_PASS8("p1024_r32x32_c8b1m2", 1024, PRad_32x32, 32, 2, 1, 32, 32),
+    FFTC_PASS8("p1024_r32x32_c8b3", 1024, PRad_32x32, 32, 1, 3, 32, 32),
 };
 
-const PassEntry* find_pass(int L, long long N) {
+// the entry of length L among a comma-separated list of candidate names
+static const PassEntry* pass_named(int L, const char* names) {
+  for (const auto& e : kPasses) {
+    if (e.L != L) continue;
+    const size_t n = strlen(e.name);
+    for (const char* q = names; q && *q;) {
+      const char* end = strchr(q, ',');
+      const size_t len = end ? (size_t)(end - q) : strlen(q);
+      if (len == n && strncmp(q, e.name, n) == 0) return &e;
+      q = end ? end + 1 : nullptr;
+    }
+  }
+  return nullptr;
+}
+
+const PassEntry* find_pass(int L, long long N, bool first) {
+  if (first)
+    if (const char* want = getenv("FFTC_PASS_FIRST"))
+      if (const PassEntry* e = pass_named(L, want)) return e;
   if (const char* want = getenv("FFTC_PASS"))
-    for (const auto& e : kPasses)
-      if (e.L == L && strcmp(e.name, want) == 0) return &e;
-  // measured on B200 (profiles/r01h): in the two-pass 2^20 plan the 1024-long pass runs
-  // fastest as one 64 KB buffer x 2 CTAs/SM (1.57 vs 1.70 ms); in the three-pass 2^27/2^28
-  // plans the double-buffered single CTA wins (2.66 vs 2.75 ms)
-  const char* pick = (L == 1024 && N > 0 && N <= (1LL << 20)) ? "p1024_r32x32_c8b1m2" : nullptr;
+    if (const PassEntry* e = pass_named(L, want)) return e;
+  // measured on B200 (profiles/r01j, tools/pass_matrix.sh): the 3-buffer ring wins for every
+  // 1024-long pass (2^20 1.58 -> 1.44 ms, 2^28 2.67 -> 2.62 ms), for the later 512-long passes
+  // (2^18 1.49 -> 1.43 ms) and for the later 256-long passes of three-pass plans (N > 2^20:
+  // 2^24 2.40 -> 2.35 ms) but not of two-pass ones (2^16 1.49 -> 1.53 ms, 2^17 1.52 ->
+  // 1.58 ms); first passes of length <= 512 keep two buffers (no TMA store to wait for)
+  const char* pick = nullptr;
+  if (L == 1024) pick = "p1024_r32x32_c8b3";
+  else if (L == 512 && !first) pick = "p512_r16x32_c8t32b3";
+  else if (L == 256 && !first && N > (1LL << 20)) pick = "p256_r16x16_b3m2";
   if (pick)
-    for (const auto& e : kPasses)
-      if (e.L == L && strcmp(e.name, pick) == 0) return &e;
+    if (const PassEntry* e = pass_named(L, pick)) return e;
   for (const auto& e : kPasses)
     if (e.L == L) return &e;
   return nullptr;

@@ -40,9 +40,10 @@ struct PassPlanData {
   int tws[kMaxPasses] = {};      // split of the pass twiddle tables (balanced: ceil(log2(Ns L) / 2))
 };
 
-// Compiled pass kernel for length L (default per L, or a measured choice for the plan's N;
-// FFTC_PASS=<name> overrides).
-const PassEntry* find_pass(int L, long long N = 0);
+// Compiled pass kernel for length L (default per L, or a measured choice for the plan's N and
+// the pass position -- first: the pass with Ns = 1; FFTC_PASS=<name>[,<name>...] overrides every
+// pass of a listed length, FFTC_PASS_FIRST=<names> the first pass only).
+const PassEntry* find_pass(int L, long long N = 0, bool first = false);
 bool passes_available();
 int pass_split(long long N, int* Ls, int max);
 cudaError_t passes_execute(const PassPlanData& pp, const float2* in, float2* out, float2* work, long long batch,

@@ -112,6 +112,24 @@ def test_every_pass_candidate(n, name, monkeypatch):
         check(gpu_fft(x, sign), x, sign)
 
 
+@pytest.mark.parametrize("n,name", [(16, "p256_r16x16_b3m2"), (24, "p256_r16x16_b3m2"), (14, "p128_r16x8_b3m4"),
+                                    (14, "p128_r16x8_b4m3"), (18, "p512_r16x32_c8t32b3"),
+                                    (20, "p1024_r32x32_c8b3"), (16, "p256_r16x16_b2m2"), (20, "p1024_r32x32_c8b2")])
+def test_pass_buffer_ring_wraps(n, name, monkeypatch):
+    """Pass kernels with 2-4 tile buffers on 2^24 elements: every persistent CTA runs many
+    tiles, so each buffer is refilled (and its mbarrier phase flips) several times; sampled
+    transforms against the oracle, both signs."""
+    monkeypatch.setenv("FFTC_PASS", name)
+    N = 1 << n
+    batch = (1 << 24) // N
+    x = synth.uniform_c64(N, batch, seed=n + 7)
+    with fftc.Plan(N, batch, -1) as p:
+        assert name in p.describe(), p.describe()
+    idx = sample_idx(batch, n_rand=3)
+    for sign in (-1, 1):
+        check(gpu_fft(x, sign)[idx], x[idx], sign)
+
+
 # ---------------------------------------------------------------- the paper's own check (P:217)
 def test_paper_protocol_p217_on_gpu():
     """The paper's accuracy experiment on the GPU path: random inputs, N = 32..1024,
