@@ -172,6 +172,13 @@ fftc_plan* fftc_plan_create_expr(const char* expr, int64_t batch, int sign);
  * len).  Returns its length, or -1 if N is not a JIT size.                 */
 int fftc_jit_source(int64_t N, char* buf, size_t len);
 
+/* Host only: the straight-line codelet `dft<R>(cf* v)` (in-place forward DFT_R
+ * of R complex values, cf = {float x, y}) that the emitter generates -- Eq. 2
+ * for composite R (Good-Thomas index maps when the split is coprime), the
+ * conjugate-pair form for primes.  2 <= R <= 128; returns its length, or -1.
+ * Truncation and NUL termination as fftc_jit_source.                       */
+int fftc_jit_codelet_source(int R, char* buf, size_t len);
+
 /* Host only (no device needed): compile the generated source with NVRTC for
  * sm_100a.  Returns the cubin size (> 0), or < 0 (-1 no NVRTC / not a JIT
  * size, -4 compile error); the NVRTC log goes to log (may be NULL).        */

@@ -73,6 +73,7 @@ def load(path: str = LIB_PATH):
         "fftc_plan_create_radices": ([i64, i64, i32, ctypes.POINTER(ctypes.c_int), i32], vp),
         "fftc_plan_create_expr": ([ctypes.c_char_p, i64, i32], vp),
         "fftc_jit_source": ([i64, ctypes.c_char_p, sz], i32),
+        "fftc_jit_codelet_source": ([ctypes.c_int, ctypes.c_char_p, sz], i32),
         "fftc_plan_create_direct": ([i64, i64, i32], vp),
         "fftc_jit_compile": ([i64, ctypes.c_char_p, sz], i32),
         "fftc_jit_pass_compile": ([i32, ctypes.c_char_p, sz], i32),
@@ -171,6 +172,15 @@ def fftc_jit_source(N: int):
         return None
     buf = ctypes.create_string_buffer(n + 1)
     load().fftc_jit_source(N, buf, n + 1)
+    return buf.value.decode()
+
+
+def fftc_jit_codelet_source(R: int):
+    n = load().fftc_jit_codelet_source(R, None, 0)
+    if n < 0:
+        return None
+    buf = ctypes.create_string_buffer(n + 1)
+    load().fftc_jit_codelet_source(R, buf, n + 1)
     return buf.value.decode()
 
 

@@ -713,6 +713,16 @@ int fftc_jit_source(int64_t N, char* buf, size_t len) {
   return (int)src.size();
 }
 
+int fftc_jit_codelet_source(int R, char* buf, size_t len) {
+  const std::string src = jit_codelet_source(R);
+  if (src.empty()) return -1;
+  if (buf && len) {
+    strncpy(buf, src.c_str(), len - 1);
+    buf[len - 1] = 0;
+  }
+  return (int)src.size();
+}
+
 int fftc_jit_compile(int64_t N, char* log, size_t loglen) {
   if (N < 2 || N > kGenericMaxN) return -1;
   std::string cubin, lg;

@@ -131,8 +131,38 @@ std::vector<std::string> emit_dft(Emitter& E, const std::vector<std::string>& x)
     }
     return y;
   }
-  // composite R = K M, Eq. 2: (DFT_K (x) I_M) D^R_M (I_K (x) DFT_M) Pi^R_K
   const int K = (R % 4 == 0 && R > 4) ? 4 : p, M = R / K;
+  int g = K, h = M;
+  while (h) {
+    const int t = g % h;
+    g = h;
+    h = t;
+  }
+  if (g == 1) {
+    // coprime K, M: Good-Thomas prime-factor form of the same DFT_R (DESIGN reading 19) --
+    // n = (n1 M + n2 K) mod R, k = (k1 eK + k2 eM) mod R with eK = 1 mod K, 0 mod M and
+    // eM = 0 mod K, 1 mod M; no internal twiddles
+    int eK = 0, eM = 0;
+    for (int t = 0; t < R; ++t) {
+      if (t % K == 1 % K && t % M == 0) eK = t;
+      if (t % K == 0 && t % M == 1 % M) eM = t;
+    }
+    std::vector<std::vector<std::string>> z((size_t)K);
+    for (int n1 = 0; n1 < K; ++n1) {
+      std::vector<std::string> sub((size_t)M);
+      for (int n2 = 0; n2 < M; ++n2) sub[n2] = x[(size_t)((n1 * M + n2 * K) % R)];
+      z[n1] = emit_dft(E, sub);
+    }
+    std::vector<std::string> y((size_t)R);
+    for (int k2 = 0; k2 < M; ++k2) {
+      std::vector<std::string> col((size_t)K);
+      for (int n1 = 0; n1 < K; ++n1) col[n1] = z[n1][k2];
+      const std::vector<std::string> o = emit_dft(E, col);
+      for (int k1 = 0; k1 < K; ++k1) y[(size_t)((k1 * eK + k2 * eM) % R)] = o[k1];
+    }
+    return y;
+  }
+  // composite R = K M, Eq. 2: (DFT_K (x) I_M) D^R_M (I_K (x) DFT_M) Pi^R_K
   std::vector<std::vector<std::string>> z((size_t)K);
   for (int r = 0; r < K; ++r) {
     std::vector<std::string> sub((size_t)M);
@@ -163,6 +193,8 @@ std::string codelet_fn(int R) {
 }
 
 }  // namespace
+
+std::string jit_codelet_source(int R) { return (R >= 2 && R <= 128) ? codelet_fn(R) : std::string(); }
 
 int jit_radices(int N, int* R, int max) {
   if (N < 2) return -1;

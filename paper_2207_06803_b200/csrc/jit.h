@@ -24,6 +24,8 @@ int jit_radices(int N, int* R, int max);
 int jit_fpb(int N);
 // Radices of a JIT pass kernel of length L: balanced groups of its prime factors.
 int jit_pass_radices(int L, int* R, int max);
+// The straight-line codelet dft<R>(cf* v) the emitter generates (2 <= R <= 128, else "").
+std::string jit_codelet_source(int R);
 // CUDA C++ source of the kernel specialised to N ("" if unsupported).
 std::string jit_source(int N);
 // NVRTC compile to an sm_100a cubin (no device needed).  0 on success.

@@ -1,4 +1,4 @@
-"""Median CUDA-event time per plan for the given sizes (batch = 2^26/N up to 4096, else 2^28/N).
+"""Median CUDA-event time per plan for the given sizes (batch = 2^26/N up to 4096, else max(1, 2^28/N)).
 Dev tool for A/B of library builds: FFTC_LIB_PATH=<variant .so> python tools/time_sizes.py N ..."""
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -6,11 +6,11 @@ import torch
 import paper_2207_06803_b200 as fftc
 
 tag = os.environ.get("TAG", os.path.basename(fftc.LIB_PATH))
-x = torch.randn(1 << 28, dtype=torch.complex64, device="cuda")
+sizes = [int(a) for a in sys.argv[1:]]
+x = torch.randn(max([1 << 28] + sizes), dtype=torch.complex64, device="cuda")
 y = torch.empty_like(x)
-for a in sys.argv[1:]:
-    N = int(a)
-    batch = ((1 << 28) if N > 4096 else (1 << 26)) // N
+for N in sizes:
+    batch = max(1, ((1 << 28) if N > 4096 else (1 << 26)) // N)
     with fftc.Plan(N, batch, -1) as p:
         for _ in range(3):
             p.execute(x, y)
