@@ -80,13 +80,90 @@ constexpr int codelet_outer(int R) {
 }
 
 // ---------------------------------------------------------------- complex helpers
-FFTC_HD float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-FFTC_HD float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+// FFTC_PACKED: on the device, complex arithmetic uses sm_100's paired FP32 instructions
+// (add/sub/mul/fma.rn.f32x2 -> FADD2 / FMUL2 / FFMA2 on a (re, im) register pair; ptxas folds
+// the component swaps and negations of +-i products and the re/im broadcasts of a complex
+// multiply into operand modifiers), about half the FP32 instructions of the scalar form.  Each
+// lane op is the same IEEE round-to-nearest operation as the scalar one; only FMA contraction
+// differs.  The host build (codelet tests) always takes the scalar form.
+#ifndef FFTC_PACKED
+#define FFTC_PACKED 0  // measured neutral on B200: FADD2 issues at ~0.4/clk per SMSP
+#endif
+#if defined(__CUDA_ARCH__) && FFTC_PACKED
+#define FFTC_PK 1
+typedef unsigned long long fftc_u64;
+__device__ __forceinline__ fftc_u64 pk2(float a, float b) {
+  fftc_u64 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 upk2(fftc_u64 r) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+  return make_float2(a, b);
+}
+__device__ __forceinline__ fftc_u64 add2(fftc_u64 a, fftc_u64 b) {
+  fftc_u64 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ fftc_u64 sub2(fftc_u64 a, fftc_u64 b) {
+  fftc_u64 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ fftc_u64 mul2(fftc_u64 a, fftc_u64 b) {
+  fftc_u64 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ fftc_u64 fma2(fftc_u64 a, fftc_u64 b, fftc_u64 c) {
+  fftc_u64 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+#else
+#define FFTC_PK 0
+#endif
+
+FFTC_HD float2 cadd(float2 a, float2 b) {
+#if FFTC_PK
+  return upk2(add2(pk2(a.x, a.y), pk2(b.x, b.y)));
+#else
+  return make_float2(a.x + b.x, a.y + b.y);
+#endif
+}
+FFTC_HD float2 csub(float2 a, float2 b) {
+#if FFTC_PK
+  return upk2(sub2(pk2(a.x, a.y), pk2(b.x, b.y)));
+#else
+  return make_float2(a.x - b.x, a.y - b.y);
+#endif
+}
+// a * b = a.x (b.x, b.y) + a.y (-b.y, b.x)
 FFTC_HD float2 cmul(float2 a, float2 b) {
+#if FFTC_PK
+  return upk2(fma2(pk2(a.y, a.y), pk2(-b.y, b.x), mul2(pk2(a.x, a.x), pk2(b.x, b.y))));
+#else
   return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+#endif
+}
+// acc + c * x for a real scalar c
+FFTC_HD float2 cfma_r(float c, float2 x, float2 acc) {
+#if FFTC_PK
+  return upk2(fma2(pk2(c, c), pk2(x.x, x.y), pk2(acc.x, acc.y)));
+#else
+  return make_float2(fmaf(c, x.x, acc.x), fmaf(c, x.y, acc.y));
+#endif
 }
 FFTC_HD float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
-FFTC_HD float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+FFTC_HD float2 cscale(float2 a, float s) {
+#if FFTC_PK
+  return upk2(mul2(pk2(a.x, a.y), pk2(s, s)));
+#else
+  return make_float2(a.x * s, a.y * s);
+#endif
+}
 // -i * a
 FFTC_HD float2 mul_mi(float2 a) { return make_float2(a.y, -a.x); }
 // +i * a
@@ -104,14 +181,18 @@ FFTC_HD float2 mul_root(float2 a) {
     if constexpr (k8 == 2) return mul_mi(a);
     else if constexpr (k8 == 4) return make_float2(-a.x, -a.y);
     else if constexpr (k8 == 6) return mul_pi(a);
-    else if constexpr (k8 == 1) return make_float2((a.x + a.y) * h, (a.y - a.x) * h);
-    else if constexpr (k8 == 3) return make_float2((a.y - a.x) * h, -(a.x + a.y) * h);
-    else if constexpr (k8 == 5) return make_float2(-(a.x + a.y) * h, (a.x - a.y) * h);
-    else return make_float2((a.x - a.y) * h, (a.x + a.y) * h);  // k8 == 7
+    else if constexpr (k8 == 1) return cscale(cadd(a, mul_mi(a)), h);  // ((x + y) h, (y - x) h)
+    else if constexpr (k8 == 3) return cscale(csub(mul_mi(a), a), h);   // ((y - x) h, -(x + y) h)
+    else if constexpr (k8 == 5) return cscale(csub(mul_pi(a), a), h);   // (-(x + y) h, (x - y) h)
+    else return cscale(cadd(a, mul_pi(a)), h);                          // k8 == 7: ((x - y) h, (x + y) h)
   } else {
     constexpr float c = float(cos2pi(e, R));
     constexpr float s = float(-sin2pi(e, R));
+#if FFTC_PK
+    return upk2(fma2(pk2(a.x, a.x), pk2(c, s), mul2(pk2(a.y, a.y), pk2(-s, c))));
+#else
     return make_float2(fmaf(a.x, c, -a.y * s), fmaf(a.x, s, a.y * c));
+#endif
   }
 }
 
@@ -173,10 +254,8 @@ struct Codelet<P, std::enable_if_t<(P > 2) && is_prime(P)>> {
         constexpr int n = decltype(n_)::value + 1;
         constexpr float c = float(cos2pi((long long)n * k, P));
         constexpr float s = float(sin2pi((long long)n * k, P));
-        A.x = fmaf(c, sp[n].x, A.x);
-        A.y = fmaf(c, sp[n].y, A.y);
-        B.x = fmaf(s, sm[n].x, B.x);
-        B.y = fmaf(s, sm[n].y, B.y);
+        A = cfma_r(c, sp[n], A);
+        B = cfma_r(s, sm[n], B);
       });
       out[k] = cadd(A, mul_mi(B));
       out[P - k] = csub(A, mul_mi(B));
