@@ -61,11 +61,17 @@ __global__ void __launch_bounds__(P::THREADS, MINB)
   if (threadIdx.x == 0)
     for (int k = 0; k < NBUF; ++k) mbar_init(&full[k], 1);
   __syncthreads();
+  // the CTA's it-th tile: groups of g.group adjacent tiles (their TMA rows share pages and DRAM
+  // rows), groups dealt round-robin over the grid; group = 1 is the plain grid stride
+  const int grp = g.group;
+  auto tile_of = [&](int i) -> long long {
+    return ((long long)(i / grp) * gridDim.x + blockIdx.x) * grp + (i % grp);
+  };
   if (threadIdx.x == 0)
     for (int k = 0; k < AHEAD; ++k)
-      if (blockIdx.x + (long long)k * gridDim.x < T) issue(blockIdx.x + (long long)k * gridDim.x, k);
+      if (tile_of(k) < T) issue(tile_of(k), k);
   int it = 0;
-  for (long long t = blockIdx.x; t < T; t += gridDim.x, ++it) {
+  for (long long t = tile_of(0); t < T; t = tile_of(++it)) {
     const int k = it % NBUF;
     float2* sm = buf0 + k * L * C;
     const int b = (int)(t / tpb), c0 = (int)(t % tpb) * C;
@@ -102,13 +108,13 @@ __global__ void __launch_bounds__(P::THREADS, MINB)
     if constexpr (RING) {
       // refill the previous tile's buffer: its store (committed one iteration ago) has had a
       // whole tile of compute to read it; the store just committed may stay in flight
-      if (threadIdx.x == 0 && t + AHEAD * (long long)gridDim.x < T) {
+      if (threadIdx.x == 0 && tile_of(it + AHEAD) < T) {
         bulk_wait_read1();
-        issue(t + AHEAD * (long long)gridDim.x, (it + AHEAD) % NBUF);
+        issue(tile_of(it + AHEAD), (it + AHEAD) % NBUF);
       }
-    } else if (threadIdx.x == 0 && t + NBUF * (long long)gridDim.x < T) {
+    } else if (threadIdx.x == 0 && tile_of(it + NBUF) < T) {
       bulk_wait_read0();  // the store has finished reading this buffer
-      issue(t + NBUF * (long long)gridDim.x, k);
+      issue(tile_of(it + NBUF), k);
     }
   }
   if (threadIdx.x == 0) bulk_wait0();
@@ -126,7 +132,8 @@ cudaError_t launch_pass(bool first, const CUtensorMap& tin, const CUtensorMap& t
   if (ks.err != cudaSuccess) return ks.err;
   const int gm = ks.grid_max;
   if (g.tiles_total == 0) return cudaSuccess;
-  const unsigned grid = (unsigned)(g.tiles_total < gm ? g.tiles_total : gm);
+  const long long groups = (g.tiles_total + g.group - 1) / g.group;
+  const unsigned grid = (unsigned)(groups < gm ? groups : gm);
   kern<<<grid, P::THREADS, smem, st>>>(tin, tout, out_first, tw, twA, twB, g, conj_in ? -1.f : 1.f,
                                       conj_out ? -1.f : 1.f);
   return cudaGetLastError();
@@ -338,6 +345,14 @@ cudaError_t passes_execute(const PassPlanData& pp, const float2* in, float2* out
     PassGeom g{};
     g.tiles_per_batch = (int)(pp.N / L / e->cols);
     g.tiles_total = batch * g.tiles_per_batch;
+    // tiles per CTA group (adjacent column tiles back to back on one CTA: their strided TMA rows
+    // share 2 MB pages and DRAM rows).  Measured on B200 (profiles/r01j/tile_groups.jsonl):
+    // 256-long and shorter passes 2 up to 2^20, 4 above (2^16 1.58 -> 1.44 ms, 2^24 2.40 ->
+    // 2.20 ms, 2^30 14.39 -> 13.13 ms); 512/1024-long passes 2, 3 from 2^28 (2^18 1.60 -> 1.51
+    // ms, 2^28 2.62 -> 2.57 ms; 3 is slower for 2^25..2^27)
+    g.group = L >= 512 ? (pp.N >= (1LL << 28) ? 3 : 2) : (pp.N > (1LL << 20) ? 4 : 2);
+    if (const char* gs = getenv(L >= 512 ? "FFTC_PASS_GROUP_LONG" : "FFTC_PASS_GROUP"))
+      g.group = atoi(gs) > 0 ? atoi(gs) : 1;
     g.Ns = (int)Ns;
     g.N = pp.N;
     g.tw = s > 0;

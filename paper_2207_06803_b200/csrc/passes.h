@@ -13,6 +13,7 @@ struct PassGeom {
   long long N;
   int tw;                 // apply the input twiddle w_{Ns L}^{(c mod Ns) r}
   int tws;                // twiddle table split: twA holds 2^tws entries
+  int group;              // a CTA walks groups of this many adjacent tiles (1 = plain grid stride)
 };
 
 typedef cudaError_t (*pass_launch_fn)(bool first, const CUtensorMap& tin, const CUtensorMap& tout, float2* out_first,
