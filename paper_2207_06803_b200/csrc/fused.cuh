@@ -69,7 +69,12 @@ struct Radices {
 //              [row i][8 columns] complex64 tile (512-byte aligned), FPB = 8.
 //   LAY_TMA128: i*16 + (((f >> 1) ^ (i & 7)) << 1 | (f & 1)) -- the TMA 128-byte swizzle of a
 //              [row i][16 columns] complex64 tile (1024-byte aligned), FPB = 16.
-enum Layout : int { LAY_AUTO = -1, LAY_SWZ = 0, LAY_FXOR = 1, LAY_ODD = 2, LAY_INTER = 3, LAY_TMA128 = 4, LAY_TMA64 = 5 };
+//   LAY_TMA16: 2- or 4-column tiles of long passes (16/32-byte TMA rows, no swizzle).  The
+//              TMA-facing layout (first reads, last writes: `lidx`) is linear, i*FPB + f; the
+//              in-between stage exchanges XOR the low log2(16/FPB) bits of i with the bits from 4
+//              up (`sidx`), which keeps the radix-16 autosort writes conflict free.
+enum Layout : int { LAY_AUTO = -1, LAY_SWZ = 0, LAY_FXOR = 1, LAY_ODD = 2, LAY_INTER = 3, LAY_TMA128 = 4, LAY_TMA64 = 5,
+                    LAY_TMA16 = 6 };
 
 constexpr int ilog2(int n) {
   int l = 0;
@@ -107,8 +112,15 @@ struct Sched {
     if constexpr (LAY == LAY_FXOR) return f * SS + (i ^ gf(f));
     else if constexpr (LAY == LAY_TMA128) return i * 16 + ((((f >> 1) ^ (i & 7)) << 1) | (f & 1));
     else if constexpr (LAY == LAY_TMA64) return i * 8 + ((((f >> 1) ^ ((i >> 1) & 3)) << 1) | (f & 1));
+    else if constexpr (LAY == LAY_TMA16) return ((i ^ ((i >> 4) & (16 / FPB - 1))) * FPB) | f;
     else if constexpr (LAY == LAY_INTER) return (i ^ ((i >> ISHIFT) & IMASK)) * FPB + f;
     else return f * SS + swz(i);
+  }
+  // position of element i of column f in the layout the TMA reads and writes (= sidx except
+  // for LAY_TMA16, whose exchanges are swizzled but whose TMA rows are linear)
+  FFTC_HD static int lidx(int f, int i) {
+    if constexpr (LAY == LAY_TMA16) return i * FPB + f;
+    else return sidx(f, i);
   }
   __device__ __forceinline__ static void sync() {
     if constexpr (WARP_SYNC) __syncwarp();

@@ -146,6 +146,12 @@ cudaError_t launch_pass(bool first, const CUtensorMap& tin, const CUtensorMap& t
 #define FFTC_PASS(NAME, L, RAD, TPF, MINB, NBUF, ...)                                                    \
   {L, RAD::S, {__VA_ARGS__}, TPF, 16, &launch_pass<Sched<L, RAD, TPF, 16, F_FAST, 0, LAY_TMA128>, MINB, NBUF>, \
    NAME}
+#define FFTC_PASS2(NAME, L, RAD, TPF, MINB, NBUF, ...)                                                  \
+  {L, RAD::S, {__VA_ARGS__}, TPF, 2, &launch_pass<Sched<L, RAD, TPF, 2, F_FAST, 0, LAY_TMA16>, MINB, NBUF>, \
+   NAME}
+#define FFTC_PASS4(NAME, L, RAD, TPF, MINB, NBUF, ...)                                                  \
+  {L, RAD::S, {__VA_ARGS__}, TPF, 4, &launch_pass<Sched<L, RAD, TPF, 4, F_FAST, 0, LAY_TMA16>, MINB, NBUF>, \
+   NAME}
 #define FFTC_PASS8(NAME, L, RAD, TPF, MINB, NBUF, ...)                                                  \
   {L, RAD::S, {__VA_ARGS__}, TPF, 8, &launch_pass<Sched<L, RAD, TPF, 8, F_FAST, 0, LAY_TMA64>, MINB, NBUF>, \
    NAME}
@@ -158,6 +164,8 @@ using PRad_16x16 = Radices<16, 16>;
 using PRad_32x16 = Radices<32, 16>;
 using PRad_16x32 = Radices<16, 32>;
 using PRad_32x32 = Radices<32, 32>;
+using PRad_16x16x8 = Radices<16, 16, 8>;
+using PRad_16x16x16 = Radices<16, 16, 16>;
 
 // First entry per length = default; FFTC_PASS=<name> pins a candidate (tuning).
 static const PassEntry kPasses[] = {
@@ -184,6 +192,10 @@ static const PassEntry kPasses[] = {
     FFTC_PASS8("p1024_r32x32_c8b1", 1024, PRad_32x32, 32, 3, 1, 32, 32),
     FFTC_PASS8("p1024_r32x32_c8b1m2", 1024, PRad_32x32, 32, 2, 1, 32, 32),
     FFTC_PASS8("p1024_r32x32_c8b3", 1024, PRad_32x32, 32, 1, 3, 32, 32),
+    FFTC_PASS2("p2048_r16x16x8_c2b3", 2048, PRad_16x16x8, 128, 2, 3, 16, 16, 8),
+    FFTC_PASS2("p4096_r16x16x16_c2b3", 4096, PRad_16x16x16, 256, 1, 3, 16, 16, 16),
+    FFTC_PASS2("p4096_r16x16x16_c2b2", 4096, PRad_16x16x16, 256, 1, 2, 16, 16, 16),
+    FFTC_PASS4("p2048_r16x16x8_c4b3", 2048, PRad_16x16x8, 128, 1, 3, 16, 16, 8),
 };
 
 // the entry of length L among a comma-separated list of candidate names
@@ -214,6 +226,7 @@ const PassEntry* find_pass(int L, long long N, bool first) {
   // 1.58 ms); first passes of length <= 512 keep two buffers (no TMA store to wait for)
   const char* pick = nullptr;
   if (L == 1024) pick = "p1024_r32x32_c8b3";
+  else if (L == 4096) pick = "p4096_r16x16x16_c2b3";
   else if (L == 512 && !first) pick = "p512_r16x32_c8t32b3";
   else if (L == 256 && !first && N > (1LL << 20)) pick = "p256_r16x16_b3m2";
   if (pick)
@@ -240,6 +253,12 @@ static encode_fn get_encode() {
   return fn;
 }
 
+// shared layout of a tile row of C complex64 columns: 128 B (C = 16) and 64 B (C = 8) rows are
+// TMA-swizzled, 16-byte rows (C = 2, the 2048/4096-long passes) are linear
+static CUtensorMapSwizzle tile_swizzle(int C) {
+  return C == 16 ? CU_TENSOR_MAP_SWIZZLE_128B : C == 8 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE;  // C = 2, 4
+}
+
 // in: a [batch][L rows][NB cols] view, box [C cols][min(L, 256) rows] (the TMA box limit)
 static bool map_in(CUtensorMap* m, const void* base, long long N, int L, int C, long long batch) {
   encode_fn enc = get_encode();
@@ -250,7 +269,7 @@ static bool map_in(CUtensorMap* m, const void* base, long long N, int L, int C, 
   cuuint32_t box[3] = {(cuuint32_t)C, (cuuint32_t)(L < 256 ? L : 256), 1};
   cuuint32_t es[3] = {1, 1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_INT64, 3, const_cast<void*>(base), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, C == 16 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, tile_swizzle(C), CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 // first-pass output: column c's L outputs contiguous at c L + k: a (k % 16, c, k / 16, batch)
@@ -276,15 +295,16 @@ static bool map_out(CUtensorMap* m, void* base, long long N, int L, int C, long 
   cuuint32_t box[4] = {(cuuint32_t)C, (cuuint32_t)(L < 256 ? L : 256), 1, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_INT64, 4, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-             C == 16 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             tile_swizzle(C), CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 bool passes_available() { return get_encode() != nullptr; }
 
 // Split N (power of two, 2^9 .. 2^48) into p passes: p = ceil(log2 N / 8) with lengths in
-// [16, 256], except that 2^17 .. 2^20 take two passes of up to 1024 and 2^25 .. 2^28 three
-// passes [<= 1024, <= 1024, 256] -- one HBM round trip fewer (measured on B200, profiles/r01h;
+// [16, 256], except that 2^17 .. 2^20 take two passes of up to 1024, 2^21 / 2^22 two passes
+// [2048 / 4096, 1024] and 2^25 .. 2^28 three passes [<= 1024, <= 1024, 256] -- one HBM round
+// trip fewer (measured on B200, profiles/r01h, r01j;
 // env FFTC_PASS_MAXLOG=8 restores the short passes).  Lengths are
 // as equal as possible, larger first.
 int pass_split(long long N, int* Ls, int max) {
@@ -299,13 +319,21 @@ int pass_split(long long N, int* Ls, int max) {
     int q = 0, sum = 0;
     for (const char* c = fl; *c && q < max;) {
       const int e = atoi(c);
-      if (e < 4 || e > 10) return -1;
+      if (e < 4 || e > 12) return -1;
       Ls[q++] = 1 << e;
       sum += e;
       while (*c && *c != ',') ++c;
       if (*c == ',') ++c;
     }
     if (sum == n) return q;
+  }
+  if ((n == 21 || n == 22) && maxlog >= 10 && max >= 2) {
+    // two passes with a 2048/4096-long FIRST pass (2-column tiles; as a later pass their
+    // 16-byte strided rows are slow): 2^21 2.26 -> 1.69 ms, 2^22 2.20 -> 1.99 ms
+    // (profiles/r01j/long_first_pass.jsonl)
+    Ls[0] = 1 << (n - 10);
+    Ls[1] = 1024;
+    return 2;
   }
   int p = (n + 7) / 8;
   if (p == 3 && n <= 2 * maxlog) p = 2;  // 2^17 .. 2^20: two passes of <= 1024

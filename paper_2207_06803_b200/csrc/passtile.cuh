@@ -60,8 +60,9 @@ __device__ __forceinline__ void pass_tile(float2* sm, int f, int lt, int c, int 
                                           const float2* __restrict__ tw, const float2* __restrict__ twA,
                                           const float2* __restrict__ twB, int tws, float csign_in,
                                           float csign_out, const PassTwPre* pre = nullptr) {
-  static_assert((P::FPB == 16 && P::LAY == LAY_TMA128) || (P::FPB == 8 && P::LAY == LAY_TMA64),
-                "pass tiles: 16 columns with the TMA 128B swizzle or 8 columns with the 64B swizzle");
+  static_assert((P::FPB == 16 && P::LAY == LAY_TMA128) || (P::FPB == 8 && P::LAY == LAY_TMA64) ||
+                    ((P::FPB == 2 || P::FPB == 4) && P::LAY == LAY_TMA16 && P::S >= 2),
+                "pass tiles: 16 columns with the TMA 128B swizzle, 8 with the 64B swizzle, or 2/4 (linear)");
   constexpr int L = P::N;
   constexpr int R0 = P::R(0);
   constexpr int NB0 = L / R0;                      // sub-stage 0: element i = j + r NB0
@@ -85,7 +86,7 @@ __device__ __forceinline__ void pass_tile(float2* sm, int f, int lt, int c, int 
   }
   float2 base = make_float2(1.f, 0.f);
   auto gload = [&](int i, int r) {
-    float2 v = sm[P::sidx(f, i)];
+    float2 v = sm[P::lidx(f, i)];
     v.y *= csign_in;
     if constexpr (TW) {
       if (r == 0) base = pre ? pre->base : root_lookup_s(twA, twB, m * i, tws);
@@ -101,7 +102,7 @@ __device__ __forceinline__ void pass_tile(float2* sm, int f, int lt, int c, int 
   // the last sub-stage writes in place (all reads precede it); OUT0: in the pass-0 store layout
   auto gstore = [&](int i, float2 v, int) {
     if constexpr (OUT0) sm[out0_idx<P>(f, i)] = make_float2(v.x, csign_out * v.y);
-    else sm[P::sidx(f, i)] = make_float2(v.x, csign_out * v.y);
+    else sm[P::lidx(f, i)] = make_float2(v.x, csign_out * v.y);
   };
   // sub-stages of DFT_L in place on the tile (every stage reads all, syncs, writes)
   sfor<P::S>([&](auto s_) {
@@ -139,7 +140,7 @@ __device__ __forceinline__ void pass0_store(const float2* sm, float2* __restrict
       constexpr int n = decltype(n_)::value;
       const int e = threadIdx.x + n * P::THREADS;
       const int r = e % L, cc = e / L;
-      st(go + cc * L + r, sm[P::sidx(cc, r)]);
+      st(go + cc * L + r, sm[P::lidx(cc, r)]);
     });
   }
 }

@@ -130,6 +130,24 @@ def test_pass_buffer_ring_wraps(n, name, monkeypatch):
         check(gpu_fft(x, sign)[idx], x[idx], sign)
 
 
+@pytest.mark.parametrize("logs", ["12,12", "11,11", "12,11", "11,10", "12,8", "8,12", "12,6,6", "11,9,4"])
+def test_long_pass_two_column_tiles(logs, monkeypatch):
+    """2048/4096-long passes (2-column tiles, 16-byte TMA rows, swizzled exchanges): forced
+    splits of 2^16..2^24, first and later positions, sampled transforms vs the oracle."""
+    monkeypatch.setenv("FFTC_PASS_LOGS", logs)
+    n = sum(int(e) for e in logs.split(","))
+    N = 1 << n
+    batch = max(1, (1 << 23) // N) | 1
+    x = synth.uniform_c64(N, batch, seed=n + 11)
+    with fftc.Plan(N, batch, -1) as p:
+        d = p.describe()
+        for e in logs.split(","):
+            assert "p%d_" % (1 << int(e)) in d, d
+    idx = sample_idx(batch, n_rand=3)
+    for sign in (-1, 1):
+        check(gpu_fft(x, sign)[idx], x[idx], sign)
+
+
 # ---------------------------------------------------------------- the paper's own check (P:217)
 def test_paper_protocol_p217_on_gpu():
     """The paper's accuracy experiment on the GPU path: random inputs, N = 32..1024,
