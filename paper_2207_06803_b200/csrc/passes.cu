@@ -76,15 +76,17 @@ __global__ void __launch_bounds__(P::THREADS, MINB)
     float2* sm = buf0 + k * L * C;
     const int b = (int)(t / tpb), c0 = (int)(t % tpb) * C;
     const int c = c0 + f;
+    // one sub-stage-0 butterfly per thread: its input twiddles are formed under the TMA wait
+    constexpr bool PRE = !FIRST && (L / P::R(0) <= P::TPF);
     PassTwPre pre{};
-    if constexpr (!FIRST) pre = pass_tw_pre<P>(c, lt, g.Ns, twA, twB, g.tws);  // under the TMA wait
+    if constexpr (PRE) pre = pass_tw_pre<P>(c, lt, g.Ns, twA, twB, g.tws);
     mbar_wait(&full[k], (it / NBUF) & 1);
     // first pass, 8-column tiles: one TMA store of the tile in the pass-0 output layout
     // (measured faster for L = 512/1024); 16-column tiles: coalesced 8-byte stores, lanes
     // walking each column's contiguous outputs (measured faster for L <= 256)
     constexpr bool TMA0 = FIRST && C == 8;
     pass_tile<P, !FIRST, TMA0>(sm, f, lt, c, g.Ns, tw, twA, twB, g.tws, csign_in, csign_out,
-                               FIRST ? nullptr : &pre);
+                               PRE ? &pre : nullptr);
     if constexpr (FIRST && !TMA0) {
       __syncthreads();
       pass0_store<P>(sm, out_first + (long long)b * g.N + (long long)c0 * L,
@@ -196,6 +198,7 @@ static const PassEntry kPasses[] = {
     FFTC_PASS2("p4096_r16x16x16_c2b3", 4096, PRad_16x16x16, 256, 1, 3, 16, 16, 16),
     FFTC_PASS2("p4096_r16x16x16_c2b2", 4096, PRad_16x16x16, 256, 1, 2, 16, 16, 16),
     FFTC_PASS4("p2048_r16x16x8_c4b3", 2048, PRad_16x16x8, 128, 1, 3, 16, 16, 8),
+    FFTC_PASS4("p4096_r16x16x16_c4b1", 4096, PRad_16x16x16, 128, 1, 1, 16, 16, 16),
 };
 
 // the entry of length L among a comma-separated list of candidate names
@@ -227,6 +230,7 @@ const PassEntry* find_pass(int L, long long N, bool first) {
   const char* pick = nullptr;
   if (L == 1024) pick = "p1024_r32x32_c8b3";
   else if (L == 4096) pick = "p4096_r16x16x16_c2b3";
+  else if (L == 2048) pick = first ? "p2048_r16x16x8_c2b3" : "p2048_r16x16x8_c4b3";
   else if (L == 512 && !first) pick = "p512_r16x32_c8t32b3";
   else if (L == 256 && !first && N > (1LL << 20)) pick = "p256_r16x16_b3m2";
   if (pick)
@@ -302,8 +306,8 @@ static bool map_out(CUtensorMap* m, void* base, long long N, int L, int C, long 
 bool passes_available() { return get_encode() != nullptr; }
 
 // Split N (power of two, 2^9 .. 2^48) into p passes: p = ceil(log2 N / 8) with lengths in
-// [16, 256], except that 2^17 .. 2^20 take two passes of up to 1024, 2^21 / 2^22 two passes
-// [2048 / 4096, 1024] and 2^25 .. 2^28 three passes [<= 1024, <= 1024, 256] -- one HBM round
+// [16, 256], except that 2^17 .. 2^20 take two passes of up to 1024, 2^21 .. 2^23 two passes
+// with 2048/4096-long ones and 2^25 .. 2^28 three passes [<= 1024, <= 1024, 256] -- one HBM round
 // trip fewer (measured on B200, profiles/r01h, r01j;
 // env FFTC_PASS_MAXLOG=8 restores the short passes).  Lengths are
 // as equal as possible, larger first.
@@ -327,12 +331,12 @@ int pass_split(long long N, int* Ls, int max) {
     }
     if (sum == n) return q;
   }
-  if ((n == 21 || n == 22) && maxlog >= 10 && max >= 2) {
-    // two passes with a 2048/4096-long FIRST pass (2-column tiles; as a later pass their
-    // 16-byte strided rows are slow): 2^21 2.26 -> 1.69 ms, 2^22 2.20 -> 1.99 ms
-    // (profiles/r01j/long_first_pass.jsonl)
-    Ls[0] = 1 << (n - 10);
-    Ls[1] = 1024;
+  if (n >= 21 && n <= 23 && maxlog >= 10 && max >= 2) {
+    // two passes with 2048/4096-long passes (2-column tiles first, 4-column tiles -- full 32-byte
+    // sectors per strided row -- later): 2^21 [2048, 1024] 2.26 -> 1.69 ms, 2^22 [2048, 2048]
+    // 2.20 -> 1.89 ms, 2^23 [4096, 2048] 2.22 -> 2.13 ms (profiles/r01j/long_first_pass.jsonl)
+    Ls[0] = n == 21 ? 2048 : n == 22 ? 2048 : 4096;
+    Ls[1] = n == 21 ? 1024 : 2048;
     return 2;
   }
   int p = (n + 7) / 8;

@@ -130,11 +130,16 @@ def test_pass_buffer_ring_wraps(n, name, monkeypatch):
         check(gpu_fft(x, sign)[idx], x[idx], sign)
 
 
-@pytest.mark.parametrize("logs", ["12,12", "11,11", "12,11", "11,10", "12,8", "8,12", "12,6,6", "11,9,4"])
-def test_long_pass_two_column_tiles(logs, monkeypatch):
-    """2048/4096-long passes (2-column tiles, 16-byte TMA rows, swizzled exchanges): forced
+@pytest.mark.parametrize("logs,later", [("12,12", None), ("11,11", None), ("11,11", "p2048_r16x16x8_c2b3"),
+                                        ("12,11", None), ("11,10", None), ("10,11", None), ("12,8", None),
+                                        ("8,12", None), ("12,6,6", None), ("11,9,4", None), ("8,11,4", None),
+                                        ("12,12", "p4096_r16x16x16_c4b1")])
+def test_long_pass_narrow_tiles(logs, later, monkeypatch):
+    """2048/4096-long passes (2/4-column tiles, 16/32-byte TMA rows, swizzled exchanges): forced
     splits of 2^16..2^24, first and later positions, sampled transforms vs the oracle."""
     monkeypatch.setenv("FFTC_PASS_LOGS", logs)
+    if later:
+        monkeypatch.setenv("FFTC_PASS", later)
     n = sum(int(e) for e in logs.split(","))
     N = 1 << n
     batch = max(1, (1 << 23) // N) | 1
@@ -461,7 +466,7 @@ def test_boundary_errors():
 def test_describe_and_launches():
     for N, kind, launches in [(64, "fused", 1), (4096, "fused", 1), (48, "generic", 1), (1 << 20, "passes", 2),
                               (1 << 24, "passes", 3), (1 << 13, "passes", 2), (1 << 16, "passes", 2),
-                              (1 << 22, "passes", 3)]:
+                              (1 << 22, "passes", 2), (1 << 23, "passes", 2)]:
         with fftc.Plan(N, 2, -1) as p:
             assert ("kind=" + kind) in p.describe()
             assert p.launches() == launches
