@@ -85,7 +85,9 @@ constexpr int ilog2(int n) {
 // Compile-time schedule of one fused transform.
 //   N: length, Rad: Radices<...>, TPF: threads per transform, FPB: transforms per CTA,
 //   MAP: thread mapping, PAD: extra elements per transform row (LAY_SWZ / LAY_ODD).
-template <int N_, class Rad, int TPF_, int FPB_, int MAP_, int PAD_ = 0, int LAY_ = LAY_AUTO>
+//   TAG: distinguishes otherwise identical schedules compiled in another translation unit with
+//   different codelet arithmetic (kernels_packed.cu), so their kernel symbols stay distinct.
+template <int N_, class Rad, int TPF_, int FPB_, int MAP_, int PAD_ = 0, int LAY_ = LAY_AUTO, int TAG_ = 0>
 struct Sched {
   static constexpr int N = N_, TPF = TPF_, FPB = FPB_, MAP = MAP_;
   static constexpr int S = Rad::S;

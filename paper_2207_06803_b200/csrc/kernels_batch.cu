@@ -6,15 +6,16 @@
 
 namespace fftc {
 
-extern const FusedEntry kTable_small[], kTable_mid[], kTable_large[], kTable_mixed[];
-extern const int kCount_small, kCount_mid, kCount_large, kCount_mixed;
+extern const FusedEntry kTable_packed[], kTable_small[], kTable_mid[], kTable_large[], kTable_mixed[];
+extern const int kCount_packed, kCount_small, kCount_mid, kCount_large, kCount_mixed;
 
 namespace {
 struct Span {
   const FusedEntry* t;
   const int* n;
 };
-const Span kSpans[] = {{kTable_small, &kCount_small}, {kTable_mid, &kCount_mid},
+// kTable_packed first: its rows are the defaults for their sizes (the first row per N wins)
+const Span kSpans[] = {{kTable_packed, &kCount_packed}, {kTable_small, &kCount_small}, {kTable_mid, &kCount_mid},
                        {kTable_large, &kCount_large}, {kTable_mixed, &kCount_mixed}};
 }  // namespace
 

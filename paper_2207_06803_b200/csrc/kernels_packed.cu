@@ -1,0 +1,29 @@
+// kernels_packed.cu -- compiled single-pass schedules whose register codelets use sm_100's
+// paired FP32 arithmetic (FFTC_PACKED, codelets.cuh: FADD2 / FMUL2 / FFMA2 on (re, im) pairs)
+// (product path).  Only the sizes where it measured faster through bench.py on B200 (DESIGN §9:
+// 105 -6 %, 210 -2 %, 1000 -3 %, 3125 -5 %, 128 -5 %); their rows come first in the registry,
+// so they are the defaults, and the scalar rows stay as candidates.  Each .cu is its own device
+// module (no -rdc), so the packed codelets never mix with the scalar ones; TAG = 1 keeps the
+// kernel symbols distinct from the scalar schedules of the same shape.
+#define FFTC_PACKED 1
+#include "kernels_common.cuh"
+
+namespace fftc {
+
+#define FFTC_ENTRY_PK(NAME, N, RAD, TPF, FPB, MAP, DIRECT, MINB, ...)                                  \
+  {N, RAD::S, {__VA_ARGS__}, TPF, FPB, TPF * FPB, DIRECT,                                             \
+   Sched<N, RAD, TPF, FPB, MAP, 0, LAY_AUTO, 1>::SMEM,                                                \
+   &launch_fused_batch<Sched<N, RAD, TPF, FPB, MAP, 0, LAY_AUTO, 1>, DIRECT, MINB>, NAME}
+
+extern const FusedEntry kTable_packed[];
+extern const int kCount_packed;
+const FusedEntry kTable_packed[] = {
+    FFTC_ENTRY_PK("n128_r8x16_t16x4d_pk", 128, Rad_8x16, 16, 4, LT_FAST, true, 16, 8, 16),
+    FFTC_ENTRY_PK("n105_r7x15_t8x16d_pk", 105, Rad_7x15, 8, 16, LT_FAST, true, 8, 7, 15),
+    FFTC_ENTRY_PK("n210_r14x15_t15x8d_pk", 210, Rad_14x15, 15, 8, LT_FAST, true, 8, 14, 15),
+    FFTC_ENTRY_PK("n1000_r10x10x10_t50x2_pk", 1000, Rad_10x10x10, 50, 2, LT_FAST, true, 6, 10, 10, 10),
+    FFTC_ENTRY_PK("n3125_r25x5x25_t128x1_pk", 3125, Rad_25x5x25, 128, 1, LT_FAST, true, 4, 25, 5, 25),
+};
+const int kCount_packed = (int)(sizeof(kTable_packed) / sizeof(kTable_packed[0]));
+
+}  // namespace fftc
