@@ -351,6 +351,7 @@ fftc_plan* fftc_plan_create(int64_t N, int64_t batch, int sign) {
       const int64_t T = Ns * Ls[s];
       p->pp.tw[s] = upload_stage_table(Ls[s], e->R, e->S, &err);
       p->pp.tws[s] = balanced_split(T);
+      p->pp.group[s] = pass_group(Ls[s], N);
       if (err == cudaSuccess) p->pp.twA[s] = upload_root_table(T, (int64_t)1 << p->pp.tws[s], 1, &err);
       if (err == cudaSuccess)
         p->pp.twB[s] = upload_root_table(T, (T >> p->pp.tws[s]) + 1, (int64_t)1 << p->pp.tws[s], &err);
@@ -564,6 +565,8 @@ int fftc_plan_describe(const fftc_plan* p, char* buf, size_t len) {
       n += snprintf(tmp + n, sizeof(tmp) - n, "kind=passes N=%lld batch=%lld sign=%d passes=", (long long)p->N,
                     (long long)p->batch, p->sign);
       for (int s = 0; s < p->pp.p; ++s) n += snprintf(tmp + n, sizeof(tmp) - n, "%s%s", s ? "," : "", p->pp.e[s]->name);
+      n += snprintf(tmp + n, sizeof(tmp) - n, " tile_groups=");
+      for (int s = 0; s < p->pp.p; ++s) n += snprintf(tmp + n, sizeof(tmp) - n, "%s%d", s ? "," : "", p->pp.group[s]);
       n += snprintf(tmp + n, sizeof(tmp) - n, " tma=tensor3d/4d workspace=%lld launches=%d",
                     (long long)(p->N * p->batch * (int64_t)sizeof(float2)), p->pp.p);
       break;

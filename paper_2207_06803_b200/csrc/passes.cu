@@ -360,6 +360,19 @@ int pass_split(long long N, int* Ls, int max) {
   return p;
 }
 
+// Tiles per CTA group for pass length L of an N-point plan (adjacent column tiles back to back
+// on one CTA: their strided TMA rows share 2 MB pages and DRAM rows).  Measured on B200
+// (profiles/r01j/tile_groups.jsonl): 256-long and shorter passes 2 up to 2^20, 4 above (2^16
+// 1.58 -> 1.44 ms, 2^24 2.40 -> 2.20 ms, 2^30 14.39 -> 13.13 ms); 512-long and longer passes
+// 2, 3 from 2^28 (2^18 1.60 -> 1.51 ms, 2^28 2.62 -> 2.57 ms; 3 is slower for 2^25..2^27).
+// Env FFTC_PASS_GROUP / FFTC_PASS_GROUP_LONG override (tuning), read at plan creation.
+int pass_group(int L, long long N) {
+  int grp = L >= 512 ? (N >= (1LL << 28) ? 3 : 2) : (N > (1LL << 20) ? 4 : 2);
+  if (const char* gs = getenv(L >= 512 ? "FFTC_PASS_GROUP_LONG" : "FFTC_PASS_GROUP"))
+    grp = atoi(gs) > 0 ? atoi(gs) : 1;
+  return grp;
+}
+
 cudaError_t passes_execute(const PassPlanData& pp, const float2* in, float2* out, float2* work, long long batch,
                            int conj, cudaStream_t st) {
   // ping-pong so the last pass lands in `out`: pass s writes out if (p-1-s) even, else work
@@ -377,14 +390,7 @@ cudaError_t passes_execute(const PassPlanData& pp, const float2* in, float2* out
     PassGeom g{};
     g.tiles_per_batch = (int)(pp.N / L / e->cols);
     g.tiles_total = batch * g.tiles_per_batch;
-    // tiles per CTA group (adjacent column tiles back to back on one CTA: their strided TMA rows
-    // share 2 MB pages and DRAM rows).  Measured on B200 (profiles/r01j/tile_groups.jsonl):
-    // 256-long and shorter passes 2 up to 2^20, 4 above (2^16 1.58 -> 1.44 ms, 2^24 2.40 ->
-    // 2.20 ms, 2^30 14.39 -> 13.13 ms); 512/1024-long passes 2, 3 from 2^28 (2^18 1.60 -> 1.51
-    // ms, 2^28 2.62 -> 2.57 ms; 3 is slower for 2^25..2^27)
-    g.group = L >= 512 ? (pp.N >= (1LL << 28) ? 3 : 2) : (pp.N > (1LL << 20) ? 4 : 2);
-    if (const char* gs = getenv(L >= 512 ? "FFTC_PASS_GROUP_LONG" : "FFTC_PASS_GROUP"))
-      g.group = atoi(gs) > 0 ? atoi(gs) : 1;
+    g.group = pp.group[s] > 0 ? pp.group[s] : 1;
     g.Ns = (int)Ns;
     g.N = pp.N;
     g.tw = s > 0;

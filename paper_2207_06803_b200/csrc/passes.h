@@ -39,6 +39,7 @@ struct PassPlanData {
   float2* twA[kMaxPasses] = {};  // w_{Ns L}^t, t < 2^tws
   float2* twB[kMaxPasses] = {};  // w_{Ns L}^{2^tws h}
   int tws[kMaxPasses] = {};      // split of the pass twiddle tables (balanced: ceil(log2(Ns L) / 2))
+  int group[kMaxPasses] = {};    // tiles per CTA group (pass_group)
 };
 
 // Compiled pass kernel for length L (default per L, or a measured choice for the plan's N and
@@ -47,6 +48,7 @@ struct PassPlanData {
 const PassEntry* find_pass(int L, long long N = 0, bool first = false);
 bool passes_available();
 int pass_split(long long N, int* Ls, int max);
+int pass_group(int L, long long N);
 cudaError_t passes_execute(const PassPlanData& pp, const float2* in, float2* out, float2* work, long long batch,
                            int conj, cudaStream_t st);
 
