@@ -6,8 +6,9 @@
 
 namespace fftc {
 
-extern const FusedEntry kTable_packed[], kTable_small[], kTable_mid[], kTable_large[], kTable_mixed[];
-extern const int kCount_packed, kCount_small, kCount_mid, kCount_large, kCount_mixed;
+extern const FusedEntry kTable_packed[], kTable_small[], kTable_mid[], kTable_large[], kTable_mixed[],
+    kTable_packed_cand[];
+extern const int kCount_packed, kCount_small, kCount_mid, kCount_large, kCount_mixed, kCount_packed_cand;
 
 namespace {
 struct Span {
@@ -16,7 +17,8 @@ struct Span {
 };
 // kTable_packed first: its rows are the defaults for their sizes (the first row per N wins)
 const Span kSpans[] = {{kTable_packed, &kCount_packed}, {kTable_small, &kCount_small}, {kTable_mid, &kCount_mid},
-                       {kTable_large, &kCount_large}, {kTable_mixed, &kCount_mixed}};
+                       {kTable_large, &kCount_large}, {kTable_mixed, &kCount_mixed},
+                       {kTable_packed_cand, &kCount_packed_cand}};
 }  // namespace
 
 int fused_count() {
