@@ -160,3 +160,14 @@ def test_invalid_args_before_device():
     assert fftc.fftc_plan_create(67 * 4096, 1, -1) == 0  # prime > 61 above the single-pass limit
     assert fftc.fftc_last_error() == fftc.FFTC_ERROR_UNSUPPORTED_SIZE
     assert fftc.fftc_execute(0, 0, 0, 0) == fftc.FFTC_ERROR_INVALID_VALUE
+
+
+def test_default_schedules_follow_the_measured_policy():
+    """The first candidate per N is the planner's default: paired-FP32 codelets exactly where
+    they measured faster on B200, the scalar schedules elsewhere."""
+    packed = {128, 105, 210, 1000, 3125, 2048}
+    for N in (8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096, 60, 105, 210, 1000, 2187, 3125):
+        names = fftc.fftc_candidates(N)
+        assert names, N
+        assert names[0].endswith("_pk") == (N in packed), (N, names[0])
+        assert len(set(names)) == len(names), N
