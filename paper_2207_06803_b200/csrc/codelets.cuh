@@ -87,7 +87,7 @@ constexpr int codelet_outer(int R) {
 // lane op is the same IEEE round-to-nearest operation as the scalar one; only FMA contraction
 // differs.  The host build (codelet tests) always takes the scalar form.
 #ifndef FFTC_PACKED
-#define FFTC_PACKED 0  // measured neutral on B200: FADD2 issues at ~0.4/clk per SMSP
+#define FFTC_PACKED 0  // per translation unit: kernels_packed.cu sets 1 (faster only where issue-bound)
 #endif
 #if defined(__CUDA_ARCH__) && FFTC_PACKED
 #define FFTC_PK 1
