@@ -443,9 +443,18 @@ fftc_status fftc_execute_host(fftc_plan* p, const void* host_in, void* host_out)
   HostStage* hs = p->hs;
   const char* hin = (const char*)host_in;
   char* hout = (char*)host_out;
+  // chunk sizes ramp up from chunk/8 and back down at the end, so the first H2D and the last
+  // D2H -- the two copies nothing overlaps -- are short (pipeline fill and drain)
+  const int64_t cmin = hs->chunk / 8 > 0 ? hs->chunk / 8 : 1;
+  int64_t ramp = cmin;
   int k = 0;
-  for (int64_t t0 = 0; t0 < p->batch && e == cudaSuccess; t0 += hs->chunk, k = (k + 1) % hs->depth) {
-    const int64_t nb = (p->batch - t0 < hs->chunk) ? p->batch - t0 : hs->chunk;
+  int64_t nb = 0;
+  for (int64_t t0 = 0; t0 < p->batch && e == cudaSuccess; t0 += nb, k = (k + 1) % hs->depth) {
+    const int64_t rem = p->batch - t0;
+    nb = ramp < hs->chunk ? ramp : hs->chunk;
+    ramp *= 2;
+    if (rem <= 2 * hs->chunk) nb = rem / 2 > cmin ? rem / 2 : cmin;  // ramp down: halves
+    if (nb > rem) nb = rem;
     const size_t bytes = (size_t)(nb * tbytes);
     e = cudaMemcpyAsync(hs->d_in[k], hin + t0 * tbytes, bytes, cudaMemcpyHostToDevice, hs->st[k]);
     if (e == cudaSuccess) e = exec_local(p, hs->d_in[k], hs->d_out[k], nb, hs->d_work[k], hs->st[k]);
