@@ -48,7 +48,9 @@ typedef enum {
   FFTC_ERROR_OUT_OF_MEMORY = 4,    /* twiddle table / workspace allocation failed */
   FFTC_ERROR_CUDA = 5,             /* CUDA launch / runtime error (cudaGetLastError captured) */
   FFTC_ERROR_NCCL = 6,             /* distributed plan: NCCL failure */
-  FFTC_ERROR_NO_DEVICE = 7         /* no CUDA device / not an sm_100 device */
+  FFTC_ERROR_NO_DEVICE = 7,        /* no CUDA device / not an sm_100 device */
+  FFTC_ERROR_WRONG_DEVICE = 8      /* execute called while a device other than the plan's is
+                                      current (a plan is bound to the device current at create) */
 } fftc_status;
 
 /* Create a plan for `batch` transforms of length N with direction `sign`.
@@ -62,10 +64,13 @@ fftc_plan* fftc_plan_create(int64_t N, int64_t batch, int sign);
 
 /* Enqueue the transform on `stream` (a cudaStream_t; NULL = legacy default
  * stream).  Asynchronous: never synchronises the host.  in/out: device
- * pointers as described above, out-of-place (in != out, no overlap).      */
+ * pointers as described above, out-of-place (in != out, no overlap).
+ * The device current on the calling thread must be the one the plan was
+ * created on (else FFTC_ERROR_WRONG_DEVICE, nothing enqueued).            */
 fftc_status fftc_execute(const fftc_plan* plan, const void* in, void* out, void* stream);
 
-/* End-to-end form of fftc_execute on HOST buffers (pinned or pageable):
+/* End-to-end form of fftc_execute on HOST buffers (pinned or pageable;
+ * the plan's device must be current, as for fftc_execute):
  * copies in -> device, runs the transform, copies the result back, in
  * chunks of transforms pipelined over two streams so host<->device copies
  * overlap the kernels.  Synchronous: returns after `out` is written.

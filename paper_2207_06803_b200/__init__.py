@@ -29,6 +29,7 @@ FFTC_ERROR_OUT_OF_MEMORY = 4
 FFTC_ERROR_CUDA = 5
 FFTC_ERROR_NCCL = 6
 FFTC_ERROR_NO_DEVICE = 7
+FFTC_ERROR_WRONG_DEVICE = 8
 FFTC_NCCL_ID_BYTES = 128
 
 _lib = None
@@ -234,6 +235,8 @@ class Plan:
 
     def __init__(self, N: int, batch: int, sign: int = -1, _handle: int | None = None):
         self.N, self.batch, self.sign = N, batch, sign
+        self.elements = N * batch  # complex64 elements of in / out per execute
+        self.device = _current_device()
         self.handle = _handle if _handle is not None else fftc_plan_create(N, batch, sign)
         if not self.handle:
             raise FFTCError(fftc_last_error(), "fftc_plan_create(N=%d, batch=%d, sign=%d)" % (N, batch, sign))
@@ -270,6 +273,8 @@ class Plan:
             raise FFTCError(fftc_last_error(), "fftc_dist_plan_create(N=%d, P=%d)" % (N, nranks))
         p = cls.__new__(cls)
         p.N, p.batch, p.sign, p.handle = N, 1, sign, h
+        p.elements = N if (loopback or nranks == 1) else N // nranks  # this rank's slab
+        p.device = _current_device()
         return p
 
     def describe(self) -> str:
@@ -278,8 +283,29 @@ class Plan:
     def launches(self) -> int:
         return fftc_plan_launches(self.handle)
 
+    def _check(self, x, out, cuda: bool):
+        import torch
+        for name, t in (("input", x), ("output", out)):
+            if hasattr(t, "data_ptr"):
+                if t.dtype != torch.complex64 or not t.is_contiguous():
+                    raise TypeError("%s: expected a contiguous complex64 tensor" % name)
+                if t.is_cuda != cuda:
+                    raise TypeError("%s: expected a %s tensor" % (name, "CUDA" if cuda else "host"))
+                if cuda and t.device.index != self.device:
+                    raise ValueError("%s is on cuda:%d, the plan on cuda:%d" % (name, t.device.index, self.device))
+                n = t.numel()
+            else:  # numpy array (host)
+                if cuda:
+                    raise TypeError("%s: expected a CUDA tensor" % name)
+                if t.dtype.name != "complex64" or not t.flags["C_CONTIGUOUS"]:
+                    raise TypeError("%s: expected a C-contiguous complex64 array" % name)
+                n = t.size
+            if n < self.elements:  # the kernels touch exactly the first `elements` elements
+                raise ValueError("%s has %d elements, the plan needs %d" % (name, n, self.elements))
+
     def execute(self, x, out, stream=None):
         import torch
+        self._check(x, out, cuda=True)
         if stream is None:
             stream = torch.cuda.current_stream(x.device).cuda_stream
         s = fftc_execute(self.handle, x.data_ptr(), out.data_ptr(), stream)
@@ -291,12 +317,15 @@ class Plan:
         import torch
         if x.dtype != torch.complex64 or not x.is_cuda or not x.is_contiguous():
             raise TypeError("expected a contiguous complex64 CUDA tensor")
+        if x.numel() < self.elements:
+            raise ValueError("input has %d elements, the plan needs %d" % (x.numel(), self.elements))
         if out is None:
             out = torch.empty_like(x)
         return self.execute(x, out)
 
     def execute_host(self, x_host, out_host):
         """End to end on host (ideally pinned) tensors/arrays: H2D, transform, D2H."""
+        self._check(x_host, out_host, cuda=False)
         s = fftc_execute_host(self.handle, _ptr(x_host), _ptr(out_host))
         if s != FFTC_SUCCESS:
             raise FFTCError(s, "fftc_execute_host")
@@ -318,6 +347,14 @@ class Plan:
 
     def __exit__(self, *a):
         self.close()
+
+
+def _current_device() -> int:
+    try:
+        import torch
+        return torch.cuda.current_device() if torch.cuda.is_available() else -1
+    except Exception:
+        return -1
 
 
 def _ptr(a) -> int:

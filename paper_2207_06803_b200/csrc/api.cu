@@ -117,6 +117,17 @@ static fftc_status from_cuda(cudaError_t e) {
   return FFTC_ERROR_CUDA;
 }
 
+static void free_host_stage(fftc::HostStage* hs) {
+  if (!hs) return;
+  for (int i = 0; i < HostStage::kDepth; ++i) {
+    cudaFree(hs->d_in[i]);
+    cudaFree(hs->d_out[i]);
+    cudaFree(hs->d_work[i]);
+    if (hs->st[i]) cudaStreamDestroy(hs->st[i]);
+  }
+  delete hs;
+}
+
 static void free_plan(fftc_plan* p) {
   if (!p) return;
   if (p->dist) dist_destroy(p->dist);
@@ -137,15 +148,7 @@ static void free_plan(fftc_plan* p) {
     cudaFree(p->pp.twA[s]);
     cudaFree(p->pp.twB[s]);
   }
-  if (p->hs) {
-    for (int i = 0; i < HostStage::kDepth; ++i) {
-      cudaFree(p->hs->d_in[i]);
-      cudaFree(p->hs->d_out[i]);
-      cudaFree(p->hs->d_work[i]);
-      if (p->hs->st[i]) cudaStreamDestroy(p->hs->st[i]);
-    }
-    delete p->hs;
-  }
+  free_host_stage(p->hs);
   delete p;
 }
 
@@ -367,7 +370,7 @@ fftc_plan* fftc_plan_create(int64_t N, int64_t batch, int sign) {
     const char* ej = getenv("FFTC_GPASS_JIT");
     const bool jit = jit_available() && !(ej && strcmp(ej, "0") == 0);
     int Lg[kMaxGPasses];
-    // JIT passes run lengths up to 1024 in place (fewer HBM passes); the compiled kernel 256
+    // JIT passes run lengths up to kJitPassMaxL = 512 (fewer HBM passes); the compiled kernel 256
     const int pg = gpass_split(N, Lg, kMaxGPasses, 7, jit ? kJitPassMaxL : kGpassMaxL);
     if (pg < 0) return fail(p, FFTC_ERROR_UNSUPPORTED_SIZE);
     int R[kMaxGPasses][kMaxStages], S[kMaxGPasses];
@@ -396,8 +399,15 @@ fftc_plan* fftc_plan_create(int64_t N, int64_t batch, int sign) {
 
 static bool misaligned(const void* a) { return ((uintptr_t)a & 15u) != 0; }
 
+// A plan's tables, workspace and kernel attributes live on the device current at create.
+static bool on_plan_device(const fftc_plan* p) {
+  int dev = -1;
+  return cudaGetDevice(&dev) == cudaSuccess && dev == p->device;
+}
+
 fftc_status fftc_execute(const fftc_plan* p, const void* in, void* out, void* stream) {
   if (!p || !in || !out) return FFTC_ERROR_INVALID_VALUE;
+  if (!on_plan_device(p)) return FFTC_ERROR_WRONG_DEVICE;
   if (p->kind == KIND_DIST) return dist_execute(p->dist, in, out, (cudaStream_t)stream);
   if (p->batch == 0) return FFTC_SUCCESS;
   const size_t bytes = (size_t)(p->N * p->batch) * sizeof(float2);
@@ -414,6 +424,7 @@ fftc_status fftc_execute(const fftc_plan* p, const void* in, void* out, void* st
 fftc_status fftc_execute_host(fftc_plan* p, const void* host_in, void* host_out) {
   if (!p || !host_in || !host_out || host_in == host_out) return FFTC_ERROR_INVALID_VALUE;
   if (p->kind == KIND_DIST) return FFTC_ERROR_INVALID_VALUE;
+  if (!on_plan_device(p)) return FFTC_ERROR_WRONG_DEVICE;
   if (p->batch == 0) return FFTC_SUCCESS;
   const int64_t tbytes = p->N * (int64_t)sizeof(float2);
   cudaError_t e = cudaSuccess;
@@ -438,7 +449,11 @@ fftc_status fftc_execute_host(fftc_plan* p, const void* host_in, void* host_out)
       if (e == cudaSuccess && p->kind == KIND_L2) e = cudaMalloc(&hs->d_work[i], l2_work_bytes(p->l2, chunk));
       if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&hs->st[i], cudaStreamNonBlocking);
     }
-    if (e != cudaSuccess) return from_cuda(e);
+    if (e != cudaSuccess) {  // leave no half-built staging area behind: the next call retries
+      free_host_stage(hs);
+      p->hs = nullptr;
+      return from_cuda(e);
+    }
   }
   HostStage* hs = p->hs;
   const char* hin = (const char*)host_in;
@@ -451,10 +466,14 @@ fftc_status fftc_execute_host(fftc_plan* p, const void* host_in, void* host_out)
   int64_t nb = 0;
   for (int64_t t0 = 0; t0 < p->batch && e == cudaSuccess; t0 += nb, k = (k + 1) % hs->depth) {
     const int64_t rem = p->batch - t0;
-    nb = ramp < hs->chunk ? ramp : hs->chunk;
-    ramp *= 2;
+    nb = ramp;
+    if (ramp < hs->chunk) ramp = 2 * ramp < hs->chunk ? 2 * ramp : hs->chunk;  // ramp up, capped
     if (rem <= 2 * hs->chunk) nb = rem / 2 > cmin ? rem / 2 : cmin;  // ramp down: halves
     if (nb > rem) nb = rem;
+    if (nb < 1 || nb > hs->chunk) {  // staging buffers hold hs->chunk transforms
+      e = cudaErrorInvalidValue;
+      break;
+    }
     const size_t bytes = (size_t)(nb * tbytes);
     e = cudaMemcpyAsync(hs->d_in[k], hin + t0 * tbytes, bytes, cudaMemcpyHostToDevice, hs->st[k]);
     if (e == cudaSuccess) e = exec_local(p, hs->d_in[k], hs->d_out[k], nb, hs->d_work[k], hs->st[k]);
@@ -482,6 +501,7 @@ const char* fftc_status_string(fftc_status s) {
     case FFTC_ERROR_CUDA: return "FFTC_ERROR_CUDA";
     case FFTC_ERROR_NCCL: return "FFTC_ERROR_NCCL";
     case FFTC_ERROR_NO_DEVICE: return "FFTC_ERROR_NO_DEVICE";
+    case FFTC_ERROR_WRONG_DEVICE: return "FFTC_ERROR_WRONG_DEVICE";
   }
   return "FFTC_UNKNOWN";
 }
@@ -604,7 +624,7 @@ int fftc_plan_split(int64_t N, int64_t* M, int64_t* K) { return top_split(N, M, 
 int fftc_plan_passes(int64_t N, int* lengths, int max) { return pass_split(N, lengths, max); }
 
 int fftc_plan_gpasses(int64_t N, int* lengths, int max) {
-  // as the plan does: JIT passes up to 1024 long when NVRTC is there, else the compiled 256
+  // as the plan does: JIT passes up to 512 long when NVRTC is there, else the compiled 256
   const char* ej = getenv("FFTC_GPASS_JIT");
   const bool jit = jit_available() && !(ej && strcmp(ej, "0") == 0);
   return gpass_split(N, lengths, max, 7, jit ? kJitPassMaxL : kGpassMaxL);

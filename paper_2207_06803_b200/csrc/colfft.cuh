@@ -120,8 +120,10 @@ static cudaError_t launch_colx(const float2* in, float2* out, const float2* tw, 
                                const float2* twB, const ColGeom& g, long long groups, int conj_in,
                                int conj_out, cudaStream_t st) {
   auto kern = k_colx<P, OUT_T, MINB>;
-  static const cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                       (int)P::SMEM);  // once, thread-safe
+  static PerDevice<cudaError_t> attr_pd;
+  const cudaError_t attr = attr_pd.get([&] {
+    return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::SMEM);
+  });
   if (attr != cudaSuccess) return attr;
   const long long grid = groups * g.tiles;
   if (grid == 0) return cudaSuccess;

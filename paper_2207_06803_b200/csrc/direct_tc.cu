@@ -254,7 +254,8 @@ cudaError_t launch_direct(const float2* in, float2* out, const float* g_img, lon
   static_assert(PER_SM * smem <= 227 * 1024, "CTAs per SM must fit in shared memory");
   auto kern = k_direct_tc<N, S>;
   // carveout 100: let PER_SM CTAs share an SM
-  static const KernelSetup ks = kernel_setup(kern, 128, smem, 100, PER_SM);
+  static PerDevice<KernelSetup> ks_pd;
+  const KernelSetup& ks = ks_pd.get([&] { return kernel_setup(kern, 128, smem, 100, PER_SM); });
   if (ks.err != cudaSuccess) return ks.err;
   const int grid_max = ks.grid_max;
   CUtensorMap ti, to;

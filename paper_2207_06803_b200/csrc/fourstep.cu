@@ -17,6 +17,7 @@
 
 #include "colfft.cuh"
 #include "fourstep.h"
+#include "launch_util.h"
 
 namespace fftc {
 
@@ -58,8 +59,10 @@ template <class P, int MINB>
 cudaError_t launch_rows(const float2* work, float2* out, const float2* tw, int M, long long N, long long batch,
                         int conj, cudaStream_t st) {
   auto kern = k_rows<P, MINB>;
-  static const cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                       (int)P::SMEM);  // once, thread-safe
+  static PerDevice<cudaError_t> attr_pd;
+  const cudaError_t attr = attr_pd.get([&] {
+    return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::SMEM);
+  });
   if (attr != cudaSuccess) return attr;
   const long long grid = batch * (M / P::FPB);
   if (grid == 0) return cudaSuccess;

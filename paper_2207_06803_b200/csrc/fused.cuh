@@ -392,8 +392,10 @@ template <class P, bool DIRECT, int MINB>
 static cudaError_t launch_fused_batch(const float2* in, float2* out, const float2* tw, long long batch,
                                       int conj, cudaStream_t st) {
   auto kern = k_fused_batch<P, DIRECT, MINB>;
-  static const cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                       (int)P::SMEM);  // once, thread-safe
+  static PerDevice<cudaError_t> attr_pd;
+  const cudaError_t attr = attr_pd.get([&] {
+    return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::SMEM);
+  });
   if (attr != cudaSuccess) return attr;
   const long long grid = (batch + P::FPB - 1) / P::FPB;
   if (grid == 0) return cudaSuccess;
@@ -476,7 +478,8 @@ template <class P, int MINB>
 static cudaError_t launch_fused_pipe(const float2* in, float2* out, const float2* tw, long long batch, int conj,
                                      cudaStream_t st) {
   auto kern = k_fused_pipe<P, MINB>;
-  static const KernelSetup ks = kernel_setup(kern, P::THREADS, P::SMEM);
+  static PerDevice<KernelSetup> ks_pd;
+  const KernelSetup& ks = ks_pd.get([&] { return kernel_setup(kern, P::THREADS, P::SMEM); });
   if (ks.err != cudaSuccess) return ks.err;
   const int grid_max = ks.grid_max;
   const long long ntiles = (batch + P::FPB - 1) / P::FPB;
@@ -562,7 +565,8 @@ static cudaError_t launch_fused_tma(const float2* in, float2* out, const float2*
                                     cudaStream_t st) {
   auto kern = k_fused_tma<P, MINB>;
   constexpr size_t smem = (size_t)((((P::SS * P::FPB) + 1) & ~1) + P::N * P::FPB) * sizeof(float2);
-  static const KernelSetup ks = kernel_setup(kern, P::THREADS, smem);
+  static PerDevice<KernelSetup> ks_pd;
+  const KernelSetup& ks = ks_pd.get([&] { return kernel_setup(kern, P::THREADS, smem); });
   if (ks.err != cudaSuccess) return ks.err;
   const int grid_max = ks.grid_max;
   const long long ntiles = (batch + P::FPB - 1) / P::FPB;

@@ -6,6 +6,7 @@
 // stage list is a kernel argument, loops are runtime, and stages ping-pong
 // between two shared-memory buffers.
 #include "genstage.cuh"
+#include "launch_util.h"
 #include "registry.h"
 
 namespace fftc {
@@ -69,8 +70,10 @@ cudaError_t launch_generic(const GenericSched& g, const float2* in, float2* out,
   int fpb = (int)(2048 / g.N);
   if (fpb < 1) fpb = 1;
   const size_t smem = (size_t)2 * fpb * g.N * sizeof(float2);
-  static const cudaError_t attr = cudaFuncSetAttribute(k_generic, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                       (int)(2 * kGenericMaxN * sizeof(float2)));  // once
+  static PerDevice<cudaError_t> attr_pd;
+  const cudaError_t attr = attr_pd.get([&] {
+    return cudaFuncSetAttribute(k_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * kGenericMaxN * sizeof(float2)));
+  });
   if (attr != cudaSuccess) return attr;
   const long long grid = (batch + fpb - 1) / fpb;
   if (grid == 0) return cudaSuccess;

@@ -18,6 +18,7 @@
 #include "colfft.cuh"
 #include "genstage.cuh"
 #include "gpass.h"
+#include "launch_util.h"
 
 namespace fftc {
 
@@ -163,8 +164,10 @@ int gpass_split(long long N, int* Ls, int max, int max_prime, int max_len) {
 
 cudaError_t gpass_execute(const GPassPlanData& d, const float2* in, float2* out, float2* work, long long batch,
                           int conj, cudaStream_t st) {
-  static const cudaError_t attr = cudaFuncSetAttribute(k_gpass, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                       (int)(2 * 256 * 17 * sizeof(float2)));  // max over L
+  static PerDevice<cudaError_t> attr_pd;
+  const cudaError_t attr = attr_pd.get([&] {
+    return cudaFuncSetAttribute(k_gpass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * 256 * 17 * sizeof(float2)));
+  });
   if (attr != cudaSuccess) return attr;
   const float2* src = in;
   for (int s = 0; s < d.p; ++s) {

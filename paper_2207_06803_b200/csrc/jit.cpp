@@ -553,7 +553,11 @@ int compile_src(const std::string& src, std::string* cubin, std::string* log) {
 const JitKernel* load_kernel(const std::string& key, const std::string& src, const char* name, size_t smem, int N,
                              int fpb, cudaError_t* err) {
   std::lock_guard<std::mutex> lk(g_mu);
-  auto it = g_cache.find(key);
+  // a loaded CUfunction belongs to the context (device) it was loaded in: cache per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const std::string dkey = key + "@" + std::to_string(dev);
+  auto it = g_cache.find(dkey);
   if (it != g_cache.end()) {
     *err = cudaSuccess;
     return it->second;
@@ -588,7 +592,7 @@ const JitKernel* load_kernel(const std::string& key, const std::string& src, con
     *err = cudaErrorInvalidValue;
     return nullptr;
   }
-  g_cache[key] = k;
+  g_cache[dkey] = k;
   *err = cudaSuccess;
   return k;
 }

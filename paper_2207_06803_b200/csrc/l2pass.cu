@@ -255,7 +255,8 @@ template <class PA, class PB, int MINB>
 cudaError_t launch_l2(const L2Params& q, cudaStream_t st) {
   constexpr size_t smem = (size_t)kStages * PA::N * 16 * sizeof(float2) + 1024;
   auto kern = k_l2<PA, PB, MINB>;
-  static const KernelSetup ks = kernel_setup(kern, kThreads, smem);
+  static PerDevice<KernelSetup> ks_pd;
+  const KernelSetup& ks = ks_pd.get([&] { return kernel_setup(kern, kThreads, smem); });
   if (ks.err != cudaSuccess) return ks.err;
   const int grid_max = ks.grid_max;
   const char* g = getenv("FFTC_L2_GRID");  // tuning

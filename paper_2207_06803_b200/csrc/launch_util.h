@@ -3,15 +3,33 @@
 #include <cuda_runtime.h>
 #include <stddef.h>
 
+#include <mutex>
+
 namespace fftc {
 
 // Dynamic shared-memory limit (and optionally the carveout) of a kernel plus its resident CTAs
-// per SM, computed once.  Callers keep the result in a function-local `static const`, so the
-// first call is thread-safe (C++11 static initialisation).  One process per GPU: the attributes
-// are set on the device current at the first call.
+// per SM, computed once per device (callers keep it in a function-local PerDevice).
 struct KernelSetup {
   cudaError_t err;
   int grid_max;  // SMs x resident CTAs per SM (persistent grids)
+};
+
+// One value per device, computed on first use on that device (thread-safe).  Kernel attributes
+// (the dynamic shared-memory opt-in) are per device: a process that drives several GPUs must set
+// them on each, so launchers keep their one-time setup in a function-local PerDevice.
+constexpr int kMaxDevices = 64;
+
+template <class T>
+struct PerDevice {
+  T v[kMaxDevices];
+  std::once_flag once[kMaxDevices];
+  template <class F>
+  const T& get(F make) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) dev = 0;
+    std::call_once(once[dev], [&] { v[dev] = make(); });
+    return v[dev];
+  }
 };
 
 template <class K>

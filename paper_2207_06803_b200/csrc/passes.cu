@@ -128,8 +128,10 @@ cudaError_t launch_pass(bool first, const CUtensorMap& tin, const CUtensorMap& t
                         int conj_out, cudaStream_t st) {
   constexpr size_t smem = (size_t)NBUF * P::N * P::FPB * sizeof(float2) + 1024;
   auto kern = first ? k_pass<P, true, MINB, NBUF> : k_pass<P, false, MINB, NBUF>;
-  static const KernelSetup ks_first = kernel_setup(k_pass<P, true, MINB, NBUF>, P::THREADS, smem);
-  static const KernelSetup ks_later = kernel_setup(k_pass<P, false, MINB, NBUF>, P::THREADS, smem);
+  static PerDevice<KernelSetup> ks_first_pd;
+  const KernelSetup& ks_first = ks_first_pd.get([&] { return kernel_setup(k_pass<P, true, MINB, NBUF>, P::THREADS, smem); });
+  static PerDevice<KernelSetup> ks_later_pd;
+  const KernelSetup& ks_later = ks_later_pd.get([&] { return kernel_setup(k_pass<P, false, MINB, NBUF>, P::THREADS, smem); });
   const KernelSetup& ks = first ? ks_first : ks_later;
   if (ks.err != cudaSuccess) return ks.err;
   const int gm = ks.grid_max;

@@ -4,8 +4,9 @@
   split chosen by libfftc's planner, exchanged by torch.distributed.all_to_all over
   gloo between two processes, matches the fp64 oracle.
 * The same algebra with P = 4 and 8 virtual ranks in one process (list exchange).
-* Batch sharding (weak scaling): each rank's seeded batch is distinct and
-  reproducible, and per-rank oracle results combine by max over ranks.
+* Batch sharding: each rank's contiguous shard of the one seeded batch
+  (drawn with PCG64.advance) equals the same rows of the one-GPU input, and the shards'
+  transforms gathered over gloo equal the unsharded result bit for bit.
 """
 import os
 import socket
@@ -115,9 +116,66 @@ def test_dist_split_properties():
     assert fftc.fftc_dist_split(11 * 4096, 2) is None
 
 
-def test_shard_seeds_distinct_and_reproducible():
-    a0 = synth.uniform_c64(64, 8, seed=synth.shard_seed(0, 0))
-    a1 = synth.uniform_c64(64, 8, seed=synth.shard_seed(0, 1))
-    assert np.array_equal(a0, synth.uniform_c64(64, 8, seed=0))
-    assert not np.array_equal(a0, a1)
-    assert np.array_equal(a1, synth.uniform_c64(64, 8, seed=synth.shard_seed(0, 1)))
+def test_shard_rows_equal_the_one_gpu_stream():
+    """A rank's batch shard, drawn with PCG64.advance, is bit-identical to the same rows of the
+    one-GPU input (SURVEY §8(c) c5 #9), for every partition used by bench.py --gpus P."""
+    for N, B in [(8, 1 << 10), (60, 1000), (105, 639), (4096, 16)]:
+        full = synth.uniform_c64(N, B, seed=0)
+        for P in (1, 2, 3, 4, 8):
+            parts = [synth.uniform_c64_rows(N, *synth.shard_range(B, r, P), seed=0) for r in range(P)]
+            assert np.array_equal(np.concatenate(parts), full), (N, B, P)
+    # a six-step slab is the same thing with N = 1 row element stride: elements [p N/P, (p+1) N/P)
+    v = synth.uniform_c64(1 << 12, 1, seed=0)[0]
+    for p in range(4):
+        slab = synth.uniform_c64_rows(1, p << 10, (p + 1) << 10, seed=0).reshape(-1)
+        assert np.array_equal(slab, v[p << 10:(p + 1) << 10])
+
+
+def test_shard_range_partition():
+    for B in (0, 1, 7, 16384, 1118481, 21474):
+        for P in (1, 2, 3, 4, 8):
+            r = [synth.shard_range(B, k, P) for k in range(P)]
+            assert r[0][0] == 0 and r[-1][1] == B
+            assert all(r[k][1] == r[k + 1][0] for k in range(P - 1))
+            sizes = [b - a for a, b in r]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def _shard_worker(rank, world, port, N, B, q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        b0, b1 = synth.shard_range(B, rank, world)
+        y = oracle.fft_ct(synth.uniform_c64_rows(N, b0, b1, seed=0), -1, nthreads=1)
+        t = torch.from_numpy(np.ascontiguousarray(y).view(np.float64).reshape(-1))
+        sizes = [(synth.shard_range(B, r, world)[1] - synth.shard_range(B, r, world)[0]) * N * 2
+                 for r in range(world)]
+        outs = [t if r == rank else torch.empty(n, dtype=torch.float64) for r, n in enumerate(sizes)]
+        for r in range(world):  # shards may differ in size by one transform: broadcast each
+            dist.broadcast(outs[r], r)
+        if rank == 0:
+            q.put(np.concatenate([o.numpy() for o in outs]).view(np.complex128).reshape(B, N))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("N,B", [(64, 96), (105, 37)])
+def test_batch_shards_gloo_world2(N, B):
+    """Batch sharding over two processes (gloo): each rank transforms its contiguous shard of the
+    one seeded batch; the gathered result equals the unsharded transform bit for bit."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_shard_worker, args=(r, 2, port, N, B, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    got = q.get(timeout=120)
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ref = oracle.fft_ct(synth.uniform_c64(N, B, seed=0), -1, nthreads=1)
+    assert np.array_equal(got, ref)

@@ -504,3 +504,65 @@ def test_determinism_bitwise():
     a = gpu_fft(x, -1)
     b = gpu_fft(x, -1)
     assert np.array_equal(a, b)
+
+
+# ---------------------------------------------------------------- negative controls of the gate
+@pytest.mark.parametrize("N", [64, 3125, 4096, 1 << 16])
+def test_check_rejects_wrong_gpu_output(N):
+    """check() (the parity gate every test and smoke() use) passes the real fftc output and
+    raises on wrong ones derived from it: one bin perturbed by 10*tol*||y||, the conjugated
+    spectrum, two bins swapped, and the output of the opposite sign (the error
+    check the gate descends from)."""
+    batch = 6
+    x = synth.uniform_c64(N, batch, seed=11)
+    y = gpu_fft(x, -1)
+    check(y, x, -1)  # positive control
+    tol = oracle.tolerance(N)
+    bad = y.copy()
+    bad[3, N // 3] += np.complex64(10 * tol * np.linalg.norm(y[3]))
+    wrong = [bad, np.conj(y)]
+    sw = y.copy()
+    sw[:, [1, N - 1]] = sw[:, [N - 1, 1]]
+    wrong.append(sw)
+    wrong.append(gpu_fft(x, +1))
+    for w in wrong:
+        with pytest.raises(AssertionError):
+            check(w, x, -1)
+
+
+def test_binding_rejects_short_and_wrong_tensors():
+    """The binding checks sizes, dtype, contiguity and device before handing bare pointers to
+    the C ABI (a short buffer would otherwise be read or written past its end)."""
+    N, batch = 256, 8
+    with fftc.Plan(N, batch, -1) as p:
+        x = torch.zeros(N * batch, dtype=torch.complex64, device="cuda")
+        with pytest.raises(ValueError):
+            p(x[: N * batch - 1])
+        with pytest.raises(ValueError):
+            p.execute(x, torch.empty(N * batch - 1, dtype=torch.complex64, device="cuda"))
+        with pytest.raises(TypeError):
+            p.execute(x, torch.empty(2 * N * batch, dtype=torch.float32, device="cuda"))
+        with pytest.raises(TypeError):
+            p.execute(x, torch.empty(2 * N * batch, dtype=torch.complex64, device="cuda")[::2])
+        with pytest.raises(TypeError):
+            p.execute(x.cpu(), torch.empty_like(x))
+        with pytest.raises(ValueError):
+            p.execute_host(np.zeros(N * batch - 1, np.complex64), np.zeros(N * batch, np.complex64))
+        with pytest.raises(TypeError):
+            p.execute_host(x, np.zeros(N * batch, np.complex64))
+        y = p(x)  # the well-formed call still works
+        assert y.numel() == N * batch
+
+
+def test_execute_host_many_chunks(monkeypatch):
+    """fftc_execute_host with 1 MiB chunks over a 128 MiB host buffer (> 64 chunks: the chunk-size
+    ramp must stay capped) equals the device execution bit for bit."""
+    monkeypatch.setenv("FFTC_HOST_CHUNK_MB", "1")
+    N, batch = 4096, 4096  # 128 MiB
+    x = synth.uniform_c64(N, batch, seed=12)
+    out = np.empty_like(x)
+    with fftc.Plan(N, batch, -1) as p:
+        p.execute_host(x, out)
+    assert np.array_equal(out, gpu_fft(x, -1))
+    idx = sample_idx(batch)
+    check(out[idx], x[idx], -1)

@@ -220,3 +220,66 @@ def test_tolerance_values():
     assert abs(oracle.tolerance(4096) - 2.4e-5) < 1e-18
     assert abs(oracle.tolerance(3125) - 2.322e-5) < 1e-8
     assert oracle.tolerance(1) == 0.0
+
+
+# ---------------------------------------------------------------- the gate metric itself
+def test_rel_l2_hand_values():
+    """oracle.rel_l2 against values computed by hand (BASELINE.json gate: per-transform
+    ||y - y_ref||_2 / ||y_ref||_2).  Row 0: y = [3+4i, 0], ref = [0, 5]: the difference is
+    [3+4i, -5], |.|^2 = 25 + 25 = 50, ||ref|| = 5 -> sqrt(50)/5 = sqrt(2) exactly."""
+    e = oracle.rel_l2(np.array([[3 + 4j, 0]]), np.array([[0, 5]]))
+    assert e.shape == (1,)
+    assert abs(e[0] - math.sqrt(2.0)) < 1e-15
+    # a pure phase error of pi/3 on every bin: |1 - e^{i pi/3}| = 2 sin(pi/6) = 1 -> exactly 1
+    ref = np.array([[1 + 1j, -2 + 0.5j, 3j, 0.25]])
+    e = oracle.rel_l2(ref * np.exp(1j * math.pi / 3), ref)
+    assert abs(e[0] - 1.0) < 1e-15
+    # sqrt, not the squared ratio: y = 2 ref -> 1 (squared would also be 1), y = 3 ref -> 2 (not 4)
+    assert abs(oracle.rel_l2(3 * ref, ref)[0] - 2.0) < 1e-15
+    # an error in the imaginary part only is counted: ref = [1, 1], y = [1, 1+i] -> 1/sqrt(2)
+    e = oracle.rel_l2(np.array([[1, 1 + 1j]]), np.array([[1, 1]]))
+    assert abs(e[0] - 1 / math.sqrt(2.0)) < 1e-15
+
+
+def test_rel_l2_is_per_row():
+    """One value per transform, not a whole-buffer norm: a wrong row next to exact rows
+    keeps its own error (a global norm would dilute 1.0 to 1/sqrt(3) here)."""
+    ref = np.array([[1, 0, 0], [0, 2, 0], [0, 0, 3]], dtype=np.complex128)
+    y = ref.copy()
+    y[1, 1] = 4  # row 1: |4 - 2| / 2 = 1
+    e = oracle.rel_l2(y, ref)
+    assert e.shape == (3,)
+    assert e[0] == 0.0 and e[2] == 0.0
+    assert abs(e[1] - 1.0) < 1e-15
+    assert e.max() == e[1]
+
+
+def test_rel_l2_zero_reference_and_dtypes():
+    # zero reference row: the absolute L2 of y (nothing to divide by), exact zero for y = 0
+    e = oracle.rel_l2(np.array([[0, 0], [3, 4j]]), np.zeros((2, 2)))
+    assert e[0] == 0.0 and abs(e[1] - 5.0) < 1e-15
+    # the GPU's complex64 output is upcast exactly before the difference: 1 + 2^-20 is exact in fp32
+    y = np.array([[1 + 2.0 ** -20]], dtype=np.complex64)
+    assert abs(oracle.rel_l2(y, np.array([[1.0]]))[0] - 2.0 ** -20) < 1e-22
+    # a 1-D pair is one transform
+    assert oracle.rel_l2(np.array([1, 1j]), np.array([1, 0])).shape == (1,)
+
+
+def test_gate_negative_controls_cpu():
+    """The gate accepts a correct fp32 FFT and rejects plausible wrong outputs.
+    Correct: numpy's single-precision FFT (pocketfft, float32) of the same input.  Wrong: one bin
+    perturbed by 10*tol*||y||, the conjugated spectrum, two bins swapped, the inverse's output."""
+    for N in (64, 1000, 4096):
+        x = synth.uniform_c64(N, 4, seed=7)
+        ref = oracle.fft_ct(x, -1)
+        tol = oracle.tolerance(N)
+        good = np.fft.fft(x.astype(np.complex64), axis=1).astype(np.complex64)
+        assert oracle.rel_l2(good, ref).max() <= tol
+        bad = good.copy()
+        bad[2, 5] += 10 * tol * np.linalg.norm(good[2])
+        assert oracle.rel_l2(bad, ref).max() > tol
+        assert oracle.rel_l2(np.conj(good), ref).max() > tol
+        sw = good.copy()
+        sw[:, [3, 7]] = sw[:, [7, 3]]
+        assert oracle.rel_l2(sw, ref).max() > tol
+        assert oracle.rel_l2(oracle.fft_ct(x, +1), ref).max() > tol
