@@ -23,6 +23,8 @@
 //            through shared memory with contiguous 128-bit copies; shared layout
 //            f*(N|1) + i (odd stride -> conflict free across transforms).
 #pragma once
+#include <type_traits>
+
 #include "codelets.cuh"
 #include "launch_util.h"
 #include "tma.cuh"
@@ -69,12 +71,17 @@ struct Radices {
 //              [row i][8 columns] complex64 tile (512-byte aligned), FPB = 8.
 //   LAY_TMA128: i*16 + (((f >> 1) ^ (i & 7)) << 1 | (f & 1)) -- the TMA 128-byte swizzle of a
 //              [row i][16 columns] complex64 tile (1024-byte aligned), FPB = 16.
+//   LAY_PAD16: f*SS + i + (i >> PSH), SS = N + (N >> PSH), PSH = log2 of 16, or of 32 when the leaf
+//              radix R_0 >= 32 (LT_FAST, N % 16 == 0): one pad element per 16 (32) elements.
+//              For the power-of-two Stockham accesses (reads j + r NB, writes o + r Ns with
+//              compile-time r) the padded position is (base of j) + (compile-time offset of r), so
+//              the addresses need no per-element XOR; lanes walking j stay bank-conflict free.
 //   LAY_TMA16: 2- or 4-column tiles of long passes (16/32-byte TMA rows, no swizzle).  The
 //              TMA-facing layout (first reads, last writes: `lidx`) is linear, i*FPB + f; the
 //              in-between stage exchanges XOR the low log2(16/FPB) bits of i with the bits from 4
 //              up (`sidx`), which keeps the radix-16 autosort writes conflict free.
 enum Layout : int { LAY_AUTO = -1, LAY_SWZ = 0, LAY_FXOR = 1, LAY_ODD = 2, LAY_INTER = 3, LAY_TMA128 = 4, LAY_TMA64 = 5,
-                    LAY_TMA16 = 6 };
+                    LAY_TMA16 = 6, LAY_PAD16 = 7 };
 
 constexpr int ilog2(int n) {
   int l = 0;
@@ -87,9 +94,19 @@ constexpr int ilog2(int n) {
 //   MAP: thread mapping, PAD: extra elements per transform row (LAY_SWZ / LAY_ODD).
 //   TAG: distinguishes otherwise identical schedules compiled in another translation unit with
 //   different codelet arithmetic (kernels_packed.cu), so their kernel symbols stay distinct.
-template <int N_, class Rad, int TPF_, int FPB_, int MAP_, int PAD_ = 0, int LAY_ = LAY_AUTO, int TAG_ = 0>
+// Schedule options (OPT bit mask; each variant is its own kernel instantiation):
+//   OPT_TW_LOAD  : every stage twiddle w_L^{m r} is loaded from the table (else r = 2^b loaded,
+//                  the other r formed as products, the default for power-of-two radices)
+//   OPT_VEC_IO   : direct HBM I/O stages assign each thread PAIRS of adjacent butterflies
+//                  (j = 2p, 2p + 1) and move both with one 128-bit load / store per r
+//   OPT_TW_SHARE : when TPF is a multiple of Ns, a thread's butterflies of a stage share
+//                  m = j mod Ns, so their twiddles are formed once per thread, not per butterfly
+enum SchedOpt : int { OPT_TW_LOAD = 1, OPT_VEC_IO = 2, OPT_TW_SHARE = 4 };
+
+template <int N_, class Rad, int TPF_, int FPB_, int MAP_, int PAD_ = 0, int LAY_ = LAY_AUTO, int TAG_ = 0,
+          int OPT_ = 0>
 struct Sched {
-  static constexpr int N = N_, TPF = TPF_, FPB = FPB_, MAP = MAP_;
+  static constexpr int N = N_, TPF = TPF_, FPB = FPB_, MAP = MAP_, OPT = OPT_;
   static constexpr int S = Rad::S;
   static constexpr int THREADS = TPF * FPB;
   static_assert(Rad::prod() == N, "radices must multiply to N");
@@ -101,7 +118,11 @@ struct Sched {
                              : (PAD_ == 0 && (N % 16 == 0 || N == 8)) ? LAY_FXOR : LAY_ODD;
   static constexpr bool FXOR = (LAY == LAY_FXOR);
   static constexpr bool SWZ = (LAY == LAY_SWZ) && ((N + PAD_) % 16 == 0);
-  static constexpr int SS = (LAY == LAY_FXOR) ? N : (LAY == LAY_ODD) ? ((N + PAD_) | 1) : (N + PAD_);
+  static_assert(LAY != LAY_PAD16 || (N % 16 == 0 && PAD_ == 0), "LAY_PAD16: N a multiple of 16");
+  // LAY_PAD16 period: the leaf stage writes j R_0 + r, conflict free when the period is R_0
+  static constexpr int PSH = (Rad::R[0] >= 32 && N % 32 == 0) ? 5 : 4;
+  static constexpr int SS = (LAY == LAY_FXOR) ? N : (LAY == LAY_ODD) ? ((N + PAD_) | 1)
+                            : (LAY == LAY_PAD16) ? (N + (N >> PSH)) : (N + PAD_);
   static constexpr size_t SMEM = size_t(LAY == LAY_INTER ? N : SS) * FPB * sizeof(float2);
   // LAY_INTER: XOR the bank bits of i (mod 16/FPB) with the bits above the leaf radix
   static constexpr int IMASK = (LAY == LAY_INTER && FPB < 16) ? (16 / FPB - 1) : 0;
@@ -116,7 +137,27 @@ struct Sched {
     else if constexpr (LAY == LAY_TMA64) return i * 8 + ((((f >> 1) ^ ((i >> 1) & 3)) << 1) | (f & 1));
     else if constexpr (LAY == LAY_TMA16) return ((i ^ ((i >> 4) & (16 / FPB - 1))) * FPB) | f;
     else if constexpr (LAY == LAY_INTER) return (i ^ ((i >> ISHIFT) & IMASK)) * FPB + f;
+    else if constexpr (LAY == LAY_PAD16) return f * SS + i + (i >> PSH);
     else return f * SS + swz(i);
+  }
+  // sidx(f, i0 + D) from pos0 = sidx(f, i0) for a compile-time D, with no per-element index math
+  // where the layout makes it linear: LAY_PAD16 when D is a multiple of the pad period, or when i0
+  // is (I0_ALIGNED) and D is any offset; LAY_SWZ when D is a multiple of 256 (bits 4..7 unchanged)
+  template <int D, bool I0_ALIGNED>
+  FFTC_HD static int sidx_plus(int f, int i0, int pos0) {
+    if constexpr (LAY == LAY_PAD16 && (D % (1 << PSH) == 0 || I0_ALIGNED)) return pos0 + D + (D >> PSH);
+    else if constexpr (LAY == LAY_SWZ && SWZ && D % 256 == 0) return pos0 + D;
+    else if constexpr ((LAY == LAY_SWZ && !SWZ) || LAY == LAY_ODD) return pos0 + D;  // f SS + i
+    else if constexpr (LAY == LAY_TMA128 && D % 8 == 0) return pos0 + D * 16;  // (i & 7) unchanged
+    else if constexpr (LAY == LAY_TMA64 && D % 8 == 0) return pos0 + D * 8;    // (i >> 1) & 3 unchanged
+    else if constexpr (LAY == LAY_TMA16 && D % 128 == 0) return pos0 + D * FPB;  // i >> 4 & (16/FPB-1) unchanged
+    else return sidx(f, i0 + D);
+  }
+  // lidx(f, i0 + D) from pos0 = lidx(f, i0), as sidx_plus (LAY_TMA16's TMA-facing rows are linear)
+  template <int D, bool I0_ALIGNED>
+  FFTC_HD static int lidx_plus(int f, int i0, int pos0) {
+    if constexpr (LAY == LAY_TMA16) return pos0 + D * FPB;
+    else return sidx_plus<D, I0_ALIGNED>(f, i0, pos0);
   }
   // position of element i of column f in the layout the TMA reads and writes (= sidx except
   // for LAY_TMA16, whose exchanges are swizzled but whose TMA rows are linear)
@@ -143,62 +184,134 @@ struct Sched {
 // buffer); DST_G: stage writes through gstore(i, v, r) (HBM, or shared memory in
 // the transposed-output column kernel: then MID_SYNC forces the in-place barrier
 // between the reads and the writes); r = the element's index within its butterfly.
+// gload2(i) / gstore2(i, a, b): elements i and i + 1 at once (OPT_VEC_IO stages only).
 // Twiddle table layout (per plan, built on the host in double): stage s occupies
 // entries [Ns-1, Ns-1 + (R-1) Ns), entry (Ns-1) + (r-1) Ns + m = w_L^{m r}.
-template <class P, int s, bool SRC_G, bool DST_G, bool MID_SYNC = false, class GL, class GS>
-__device__ __forceinline__ void stage(float2* sm, int f, int lt, bool fvalid,
-                                      const float2* __restrict__ tw, GL&& gload, GS&& gstore) {
+template <class P, int s, bool SRC_G, bool DST_G, bool MID_SYNC, class GL, class GS, class GL2, class GS2>
+__device__ __forceinline__ void stage_io(float2* sm, int f, int lt, bool fvalid, const float2* __restrict__ tw,
+                                         GL&& gload, GS&& gstore, GL2&& gload2, GS2&& gstore2) {
   constexpr int R = P::R(s);
   constexpr int NB = P::N / R;
   constexpr int Ns = P::ns(s);
   constexpr int L = Ns * R;
   constexpr int KB = (NB + P::TPF - 1) / P::TPF;
   constexpr bool EXACT = (NB % P::TPF) == 0;
+  // paired mapping for a direct-I/O stage: thread lt, pair k/2 -> butterflies j = 2p, 2p + 1
+  constexpr bool VEC = (P::OPT & OPT_VEC_IO) && (SRC_G || DST_G) && (KB % 2 == 0) && (NB % (2 * P::TPF) == 0) &&
+                      (!DST_G || Ns % 2 == 0);
+  // butterflies of one thread share m = j mod Ns (strided mapping, TPF a multiple of Ns)
+  constexpr bool SHARE = (P::OPT & OPT_TW_SHARE) && !VEC && s > 0 && KB > 1 && (P::TPF % Ns == 0);
+  constexpr bool LOAD_ALL = (P::OPT & OPT_TW_LOAD) || (kTwLoadAll && (R & (R - 1)) != 0);
+  auto bfly = [&](int k) { return VEC ? 2 * (lt + (k >> 1) * P::TPF) + (k & 1) : lt + k * P::TPF; };
   float2 v[KB][R];
-  sfor<KB>([&](auto k_) {
-    constexpr int k = decltype(k_)::value;
-    const int j = lt + k * P::TPF;
-    if (fvalid && (EXACT || j < NB)) {
-      sfor<R>([&](auto r_) {
-        constexpr int r = decltype(r_)::value;
-        const int i = j + r * NB;
-        if constexpr (SRC_G) v[k][r] = gload(i, r);
-        else v[k][r] = sm[P::sidx(f, i)];
+  if constexpr (VEC && SRC_G) {
+    sfor<KB / 2>([&](auto k_) {
+      constexpr int k = 2 * decltype(k_)::value;
+      const int j = bfly(k);
+      if (fvalid)
+        sfor<R>([&](auto r_) {
+          constexpr int r = decltype(r_)::value;
+          const float4 q = gload2(j + r * NB);
+          v[k][r] = make_float2(q.x, q.y);
+          v[k + 1][r] = make_float2(q.z, q.w);
+        });
+    });
+  } else {
+    sfor<KB>([&](auto k_) {
+      constexpr int k = decltype(k_)::value;
+      const int j = bfly(k);
+      if (fvalid && (EXACT || j < NB)) {
+        constexpr bool GPOS = SRC_G && std::is_invocable_v<GL, int, int, int>;  // gload(i, r, lidx position)
+        const int p0 = SRC_G ? (GPOS ? P::lidx(f, j) : 0) : P::sidx(f, j);
+        sfor<R>([&](auto r_) {
+          constexpr int r = decltype(r_)::value;
+          const int i = j + r * NB;
+          if constexpr (GPOS) v[k][r] = gload(i, r, P::template lidx_plus<r * NB, false>(f, j, p0));
+          else if constexpr (SRC_G) v[k][r] = gload(i, r);
+          else v[k][r] = sm[P::template sidx_plus<r * NB, false>(f, j, p0)];
+        });
+      }
+    });
+  }
+  if constexpr ((!SRC_G && !DST_G) || MID_SYNC) P::sync();
+  // w_L^{m r}: power-of-two radices load r = 1, 2, 4, 8, ... from the table and form every other
+  // r as the product w^{2^b} w^{r - 2^b} (at most log2(R)-1 roundings deep); LOAD_ALL loads all
+  auto twiddles = [&](int m, float2* w) {
+    const float2* t = tw + (Ns - 1) + m;
+    sfor<R - 1>([&](auto r_) {
+      constexpr int r = decltype(r_)::value + 1;
+      constexpr int hb = highbit(r);
+      if constexpr (LOAD_ALL || hb == r) w[r] = __ldg(t + (r - 1) * Ns);
+      else w[r] = cmul(w[hb], w[r - hb]);
+    });
+  };
+  if constexpr (SHARE) {
+    if (fvalid) {
+      float2 w[R];
+      twiddles(lt % Ns, w);
+      sfor<KB>([&](auto k_) {
+        constexpr int k = decltype(k_)::value;
+        if (EXACT || bfly(k) < NB)
+          sfor<R - 1>([&](auto r_) {
+            constexpr int r = decltype(r_)::value + 1;
+            v[k][r] = cmul(v[k][r], w[r]);
+          });
       });
     }
-  });
-  if constexpr ((!SRC_G && !DST_G) || MID_SYNC) P::sync();
+  }
   sfor<KB>([&](auto k_) {
     constexpr int k = decltype(k_)::value;
-    const int j = lt + k * P::TPF;
+    const int j = bfly(k);
     if (fvalid && (EXACT || j < NB)) {
       const int m = (Ns == 1) ? 0 : (j % Ns);
-      if constexpr (s > 0) {
-        // w_L^{m r}: power-of-two radices load r = 1, 2, 4, 8, ... from the table and form
-        // every other r as the product w^{2^b} w^{r - 2^b} (at most log2(R)-1 roundings deep);
-        // other radices load every r (the table holds them all): one load instead of a
-        // 4-instruction complex product, for the issue-bound odd-radix sizes
-        constexpr bool LOAD_ALL = kTwLoadAll && (R & (R - 1)) != 0;
-        const float2* t = tw + (Ns - 1) + m;
+      if constexpr (s > 0 && !SHARE) {
         float2 w[R];
+        twiddles(m, w);
         sfor<R - 1>([&](auto r_) {
           constexpr int r = decltype(r_)::value + 1;
-          constexpr int hb = highbit(r);
-          if constexpr (LOAD_ALL || hb == r) w[r] = __ldg(t + (r - 1) * Ns);
-          else w[r] = cmul(w[hb], w[r - hb]);
           v[k][r] = cmul(v[k][r], w[r]);
         });
       }
       Codelet<R>::run(v[k]);
-      const int o = (Ns == 1) ? j * R : ((j / Ns) * L + m);
-      sfor<R>([&](auto r_) {
-        constexpr int r = decltype(r_)::value;
-        if constexpr (DST_G) gstore(o + r * Ns, v[k][r], r);
-        else sm[P::sidx(f, o + r * Ns)] = v[k][r];
-      });
+      if constexpr (!(VEC && DST_G)) {
+        const int o = (Ns == 1) ? j * R : ((j / Ns) * L + m);
+        // o = j R is a multiple of the LAY_PAD16 period when R is
+        constexpr bool OALIGNED = (Ns == 1) && (R % (1 << P::PSH) == 0);
+        constexpr bool SPOS = DST_G && std::is_invocable_v<GS, int, float2, int, int>;  // gstore(i, v, r, lidx pos)
+        const int q0 = DST_G ? (SPOS ? P::lidx(f, o) : 0) : P::sidx(f, o);
+        sfor<R>([&](auto r_) {
+          constexpr int r = decltype(r_)::value;
+          if constexpr (SPOS) gstore(o + r * Ns, v[k][r], r, P::template lidx_plus<r * Ns, OALIGNED>(f, o, q0));
+          else if constexpr (DST_G) gstore(o + r * Ns, v[k][r], r);
+          else sm[P::template sidx_plus<r * Ns, OALIGNED>(f, o, q0)] = v[k][r];
+        });
+      }
     }
   });
+  if constexpr (VEC && DST_G) {
+    // the pair's outputs o + r Ns and o + 1 + r Ns are adjacent when Ns > 1 (m and m + 1 < Ns)
+    static_assert(Ns % 2 == 0, "paired stores need an even Ns");
+    sfor<KB / 2>([&](auto k_) {
+      constexpr int k = 2 * decltype(k_)::value;
+      const int j = bfly(k);
+      if (fvalid) {
+        const int o = (j / Ns) * L + (j % Ns);
+        sfor<R>([&](auto r_) {
+          constexpr int r = decltype(r_)::value;
+          gstore2(o + r * Ns, v[k][r], v[k + 1][r]);
+        });
+      }
+    });
+  }
   if constexpr (!DST_G) P::sync();
+}
+
+template <class P, int s, bool SRC_G, bool DST_G, bool MID_SYNC = false, class GL, class GS>
+__device__ __forceinline__ void stage(float2* sm, int f, int lt, bool fvalid, const float2* __restrict__ tw,
+                                      GL&& gload, GS&& gstore) {
+  stage_io<P, s, SRC_G, DST_G, MID_SYNC>(
+      sm, f, lt, fvalid, tw, gload, gstore, [](int) { return make_float4(0.f, 0.f, 0.f, 0.f); },
+      [](int, float2, float2) {});
 }
 
 // All S stages.  SRC0_G: stage 0 reads HBM; DSTL_G: the last stage writes through
@@ -210,6 +323,15 @@ __device__ __forceinline__ void run_stages(float2* sm, int f, int lt, bool fvali
     constexpr int s = decltype(s_)::value;
     stage<P, s, SRC0_G && s == 0, DSTL_G && s == P::S - 1, LAST_MID && s == P::S - 1>(sm, f, lt, fvalid, tw, gload,
                                                                                         gstore);
+  });
+}
+
+template <class P, class GL, class GS, class GL2, class GS2>
+__device__ __forceinline__ void run_stages_io(float2* sm, int f, int lt, bool fvalid, const float2* __restrict__ tw,
+                                              GL&& gload, GS&& gstore, GL2&& gload2, GS2&& gstore2) {
+  sfor<P::S>([&](auto s_) {
+    constexpr int s = decltype(s_)::value;
+    stage_io<P, s, s == 0, s == P::S - 1, false>(sm, f, lt, fvalid, tw, gload, gstore, gload2, gstore2);
   });
 }
 
@@ -370,13 +492,20 @@ __global__ void __launch_bounds__(P::THREADS, MINB)
     static_assert(P::MAP == LT_FAST, "direct I/O needs the LT_FAST mapping");
     const float2* gi = gin + (long long)f * P::N;
     float2* go = gout + (long long)f * P::N;
-    run_stages<P, true, true>(
+    run_stages_io<P>(
         sm, f, lt, fvalid, tw,
         [&](int i, int) {
           float2 a = __ldcs(gi + i);
           return make_float2(a.x, csign * a.y);
         },
-        [&](int i, float2 v, int) { __stcs(go + i, make_float2(v.x, csign * v.y)); });
+        [&](int i, float2 v, int) { __stcs(go + i, make_float2(v.x, csign * v.y)); },
+        [&](int i) {  // OPT_VEC_IO: i even, the row 16-byte aligned (N even, checked base)
+          float4 q = __ldcs(reinterpret_cast<const float4*>(gi + i));
+          return make_float4(q.x, csign * q.y, q.z, csign * q.w);
+        },
+        [&](int i, float2 a, float2 b) {
+          __stcs(reinterpret_cast<float4*>(go + i), make_float4(a.x, csign * a.y, b.x, csign * b.y));
+        });
   } else {
     tile_in<P>(sm, gin, nf, csign);
     __syncthreads();

@@ -14,6 +14,16 @@ namespace fftc {
   {N, RAD::S, {__VA_ARGS__}, TPF, FPB, TPF * FPB, true,                                        \
    Sched<N, RAD, TPF, FPB, LT_FAST, PAD>::SMEM, &launch_fused_batch<Sched<N, RAD, TPF, FPB, LT_FAST, PAD>, true, MINB>, \
    NAME}
+// LT_FAST direct schedule with SchedOpt options (fused.cuh: OPT_TW_LOAD, OPT_VEC_IO, OPT_TW_SHARE)
+#define FFTC_ENTRY_OPT(NAME, N, RAD, TPF, FPB, MINB, OPT, ...)                                     \
+  {N, RAD::S, {__VA_ARGS__}, TPF, FPB, TPF * FPB, true,                                          \
+   Sched<N, RAD, TPF, FPB, LT_FAST, 0, LAY_AUTO, 0, OPT>::SMEM,                                   \
+   &launch_fused_batch<Sched<N, RAD, TPF, FPB, LT_FAST, 0, LAY_AUTO, 0, OPT>, true, MINB>, NAME}
+// LT_FAST direct schedule with the padded shared layout (LAY_PAD16) and SchedOpt options
+#define FFTC_ENTRY_P16(NAME, N, RAD, TPF, FPB, MINB, OPT, ...)                                     \
+  {N, RAD::S, {__VA_ARGS__}, TPF, FPB, TPF * FPB, true,                                          \
+   Sched<N, RAD, TPF, FPB, LT_FAST, 0, LAY_PAD16, 0, OPT>::SMEM,                                  \
+   &launch_fused_batch<Sched<N, RAD, TPF, FPB, LT_FAST, 0, LAY_PAD16, 0, OPT>, true, MINB>, NAME}
 // persistent, TMA-fed variant (LT_FAST schedules)
 #define FFTC_TMA(NAME, N, RAD, TPF, FPB, MINB, ...)                                               \
   {N, RAD::S, {__VA_ARGS__}, TPF, FPB, TPF * FPB, 2, Sched<N, RAD, TPF, FPB, LT_FAST>::SMEM * 2,    \

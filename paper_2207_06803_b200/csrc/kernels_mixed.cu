@@ -32,6 +32,13 @@ const FusedEntry kTable_mixed[] = {
     FFTC_ENTRY("n1000_r25x40_t40x4", 1000, Rad_25x40, 40, 4, LT_FAST, true, 4, 25, 40),
     FFTC_ENTRY("n210_r15x14_t15x8", 210, Rad_15x14, 15, 8, F_FAST, false, 8, 15, 14),
     FFTC_ENTRY("n210_r15x14_t15x16", 210, Rad_15x14, 15, 16, F_FAST, false, 4, 15, 14),
+    // round 2: shared stage twiddles (TPF % Ns == 0), paired 128-bit I/O (even N), all twiddles loaded
+    FFTC_ENTRY_OPT("n2187_r27x9x9_t81x2_sh", 2187, Rad_27x9x9, 81, 2, 3, OPT_TW_SHARE, 27, 9, 9),
+    FFTC_ENTRY_OPT("n2187_r27x9x9_t81x2_shl", 2187, Rad_27x9x9, 81, 2, 3, OPT_TW_SHARE | OPT_TW_LOAD, 27, 9, 9),
+    FFTC_ENTRY_OPT("n2187_r27x9x9_t128x1_l", 2187, Rad_27x9x9, 128, 1, 4, OPT_TW_LOAD, 27, 9, 9),
+    FFTC_ENTRY_OPT("n3125_r25x5x25_t125x2_sh", 3125, Rad_25x5x25, 125, 2, 3, OPT_TW_SHARE, 25, 5, 25),
+    FFTC_ENTRY_OPT("n1000_r10x10x10_t50x2_vsh", 1000, Rad_10x10x10, 50, 2, 6, OPT_VEC_IO | OPT_TW_SHARE, 10, 10, 10),
+    FFTC_ENTRY_OPT("n1000_r10x10x10_t100x2_v", 1000, Rad_10x10x10, 100, 2, 4, OPT_VEC_IO, 10, 10, 10),
     FFTC_ENTRY("n1000_r10x10x10_t100x1", 1000, Rad_10x10x10, 100, 1, LT_FAST, true, 8, 10, 10, 10),
     FFTC_ENTRY("n2187_r3x27x27_t81x1", 2187, Rad_3x27x27, 81, 1, LT_FAST, true, 6, 3, 27, 27),
     FFTC_ENTRY("n3125_r25x25x5_t125x1", 3125, Rad_25x25x5, 125, 1, LT_FAST, true, 5, 25, 25, 5),

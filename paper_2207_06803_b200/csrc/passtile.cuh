@@ -84,25 +84,32 @@ __device__ __forceinline__ void pass_tile(float2* sm, int f, int lt, int c, int 
       });
     }
   }
-  float2 base = make_float2(1.f, 0.f);
-  auto gload = [&](int i, int r) {
-    float2 v = sm[P::lidx(f, i)];
+  // input twiddles of one butterfly, formed as a tree: w[0] = base, w[r] = w[r - 2^b] sp[b]
+  // (2^b = highest bit of r) -- one complex product per r, and the same product chain (lowest
+  // bits first) as multiplying base by sp[b] for every set bit b of r
+  float2 wt[R0];
+  auto gload = [&](int i, int r, int pos) {
+    float2 v = sm[pos];
     v.y *= csign_in;
     if constexpr (TW) {
-      if (r == 0) base = pre ? pre->base : root_lookup_s(twA, twB, m * i, tws);
-      float2 w = base;
-      sfor<NB2>([&](auto b_) {
-        constexpr int bb = decltype(b_)::value;
-        if (r & (1 << bb)) w = cmul(w, sp[bb]);
-      });
-      v = cmul(v, w);
+      if (r == 0) {
+        wt[0] = pre ? pre->base : root_lookup_s(twA, twB, m * i, tws);
+      } else {
+        int hb = 1, b = 0;
+        while (2 * hb <= r) {
+          hb *= 2;
+          ++b;
+        }
+        wt[r] = cmul(wt[r - hb], sp[b]);
+      }
+      v = cmul(v, wt[r]);
     }
     return v;
   };
   // the last sub-stage writes in place (all reads precede it); OUT0: in the pass-0 store layout
-  auto gstore = [&](int i, float2 v, int) {
+  auto gstore = [&](int i, float2 v, int, int pos) {
     if constexpr (OUT0) sm[out0_idx<P>(f, i)] = make_float2(v.x, csign_out * v.y);
-    else sm[P::lidx(f, i)] = make_float2(v.x, csign_out * v.y);
+    else sm[pos] = make_float2(v.x, csign_out * v.y);
   };
   // sub-stages of DFT_L in place on the tile (every stage reads all, syncs, writes)
   sfor<P::S>([&](auto s_) {
