@@ -533,6 +533,83 @@ static cudaError_t launch_fused_batch(const float2* in, float2* out, const float
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- warp-shuffle exchange (A/B variant)
+// N = R * R with TPF = R lanes per transform (R <= 32, a power of two), two Stockham stages.
+// Stage 0's butterfly j = lt writes positions R lt + r; stage 1's butterfly j = lt reads
+// positions lt + R r = element lt of lane r: the exchange is an R x R transpose across the
+// transform's R lanes, done here in registers by log2(R) shfl.xor rounds (round mask m: each lane
+// keeps the elements whose index bit m equals its own lane bit and swaps the other half with lane
+// lt ^ m) instead of through shared memory.  Same twiddles, codelets and order of arithmetic as
+// the shared-memory kernel, so the results are bit-identical; no shared memory, no barrier.
+template <int R>
+__device__ __forceinline__ void lane_transpose(float2 (&v)[R], int lt) {
+  sfor<ilog2(R)>([&](auto b_) {
+    constexpr int m = 1 << decltype(b_)::value;
+    const bool hi = (lt & m) != 0;
+    sfor<R>([&](auto r_) {
+      constexpr int r = decltype(r_)::value;
+      if constexpr ((r & m) == 0) {
+        const float2 send = hi ? v[r] : v[r | m];
+        float2 recv;
+        recv.x = __shfl_xor_sync(0xffffffffu, send.x, m);
+        recv.y = __shfl_xor_sync(0xffffffffu, send.y, m);
+        if (hi) v[r] = recv;
+        else v[r | m] = recv;
+      }
+    });
+  });
+}
+
+template <class P, int MINB>
+__global__ void __launch_bounds__(P::THREADS, MINB)
+    k_fused_shfl(const float2* __restrict__ in, float2* __restrict__ out, const float2* __restrict__ tw,
+                 long long batch, float csign) {
+  constexpr int R = P::R(0);
+  static_assert(P::S == 2 && P::R(1) == R && P::TPF == R && R <= 32 && (R & (R - 1)) == 0 && P::MAP == LT_FAST,
+                "shuffle exchange: N = R x R, R lanes per transform");
+  int f, lt;
+  P::thread_coords(threadIdx.x, f, lt);
+  const long long t = (long long)blockIdx.x * P::FPB + f;
+  // every lane of a transform group takes part in the shuffles; only valid transforms touch HBM
+  const bool valid = t < batch;
+  const float2* gi = in + (valid ? t : 0) * P::N;
+  float2* go = out + (valid ? t : 0) * P::N;
+  float2 v[R];
+  sfor<R>([&](auto r_) {
+    constexpr int r = decltype(r_)::value;
+    const float2 a = valid ? __ldcs(gi + lt + r * R) : make_float2(0.f, 0.f);
+    v[r] = make_float2(a.x, csign * a.y);
+  });
+  Codelet<R>::run(v);
+  lane_transpose<R>(v, lt);
+  // stage 1 (Ns = R, m = lt): w_N^{lt r}, r = 2^b loaded, the others formed as products
+  const float2* tp = tw + (R - 1) + lt;
+  float2 w[R];
+  sfor<R - 1>([&](auto r_) {
+    constexpr int r = decltype(r_)::value + 1;
+    constexpr int hb = highbit(r);
+    if constexpr (hb == r) w[r] = __ldg(tp + (r - 1) * R);
+    else w[r] = cmul(w[hb], w[r - hb]);
+    v[r] = cmul(v[r], w[r]);
+  });
+  Codelet<R>::run(v);
+  if (valid)
+    sfor<R>([&](auto r_) {
+      constexpr int r = decltype(r_)::value;
+      __stcs(go + lt + r * R, make_float2(v[r].x, csign * v[r].y));
+    });
+}
+
+template <class P, int MINB>
+static cudaError_t launch_fused_shfl(const float2* in, float2* out, const float2* tw, long long batch, int conj,
+                                     cudaStream_t st) {
+  const long long grid = (batch + P::FPB - 1) / P::FPB;
+  if (grid == 0) return cudaSuccess;
+  if (grid > 0x7fffffffLL) return cudaErrorInvalidValue;
+  k_fused_shfl<P, MINB><<<(unsigned)grid, P::THREADS, 0, st>>>(in, out, tw, batch, conj ? -1.0f : 1.0f);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- persistent register-pipelined kernel
 // LT_FAST direct schedules.  Each CTA loops over tiles of FPB transforms; the stage-0 inputs of
 // the CTA's NEXT tile are loaded into registers (plain coalesced loads, the same lanes and

@@ -24,6 +24,10 @@ namespace fftc {
   {N, RAD::S, {__VA_ARGS__}, TPF, FPB, TPF * FPB, true,                                          \
    Sched<N, RAD, TPF, FPB, LT_FAST, 0, LAY_PAD16, 0, OPT>::SMEM,                                  \
    &launch_fused_batch<Sched<N, RAD, TPF, FPB, LT_FAST, 0, LAY_PAD16, 0, OPT>, true, MINB>, NAME}
+// warp-shuffle exchange variant (N = R x R, TPF = R; fused.cuh k_fused_shfl), no shared memory
+#define FFTC_SHFL(NAME, N, RAD, TPF, FPB, MINB, ...)                                               \
+  {N, RAD::S, {__VA_ARGS__}, TPF, FPB, TPF * FPB, true, 0,                                        \
+   &launch_fused_shfl<Sched<N, RAD, TPF, FPB, LT_FAST>, MINB>, NAME}
 // persistent, TMA-fed variant (LT_FAST schedules)
 #define FFTC_TMA(NAME, N, RAD, TPF, FPB, MINB, ...)                                               \
   {N, RAD::S, {__VA_ARGS__}, TPF, FPB, TPF * FPB, 2, Sched<N, RAD, TPF, FPB, LT_FAST>::SMEM * 2,    \

@@ -19,6 +19,9 @@ const FusedEntry kTable_mid[] = {
     FFTC_ENTRY("n1024_r32x32_t32x8", 1024, Rad_32x32, 32, 8, LT_FAST, true, 2, 32, 32),
     FFTC_ENTRY("n512_r32x16_t16x4", 512, Rad_32x16, 16, 4, LT_FAST, true, 8, 32, 16),
     FFTC_ENTRY("n1024_r32x32_t32x2", 1024, Rad_32x32, 32, 2, LT_FAST, true, 8, 32, 32),
+    FFTC_SHFL("n256_r16x16_t16x8_shfl", 256, Rad_16x16, 16, 8, 8, 16, 16),
+    FFTC_SHFL("n256_r16x16_t16x16_shfl", 256, Rad_16x16, 16, 16, 4, 16, 16),
+    FFTC_SHFL("n1024_r32x32_t32x4_shfl", 1024, Rad_32x32, 32, 4, 4, 32, 32),
     FFTC_ENTRY_P16("n1024_r32x32_t32x4_p16", 1024, Rad_32x32, 32, 4, 4, 0, 32, 32),
     FFTC_ENTRY_P16("n512_r32x16_t16x8_p16", 512, Rad_32x16, 16, 8, 4, 0, 32, 16),
     FFTC_ENTRY_P16("n256_r16x16_t16x8_p16", 256, Rad_16x16, 16, 8, 8, 0, 16, 16),
