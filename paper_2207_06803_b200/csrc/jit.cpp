@@ -122,9 +122,19 @@ std::vector<std::string> emit_dft(Emitter& E, const std::vector<std::string>& x)
         by = "fmaf(" + d[j] + ".y, " + flit(sin(th)) + ", " + by + ")";
       }
       E.line("const cf " + A + " = cf{" + ax + ", " + ay + "};");
-      E.line("const cf " + B + " = cf{" + bx + ", " + by + "};");
       y[k] = E.fresh();
       y[R - k] = E.fresh();
+      if (h == 1) {
+        // R = 3: the single sine term folded into the outputs (one FMA per component, as the
+        // compiled Codelet<3>)
+        const std::string sn = flit(sin(2.0 * M_PI * (double)k / (double)R));
+        E.line("const cf " + y[k] + " = cf{fmaf(" + d[1] + ".y, " + sn + ", " + A + ".x), fmaf(" + d[1] + ".x, -" + sn +
+               ", " + A + ".y)};");
+        E.line("const cf " + y[R - k] + " = cf{fmaf(" + d[1] + ".y, -" + sn + ", " + A + ".x), fmaf(" + d[1] + ".x, " +
+               sn + ", " + A + ".y)};");
+        continue;
+      }
+      E.line("const cf " + B + " = cf{" + bx + ", " + by + "};");
       // y_k = A - i B, y_{R-k} = A + i B
       E.line("const cf " + y[k] + " = cf{" + A + ".x + " + B + ".y, " + A + ".y - " + B + ".x};");
       E.line("const cf " + y[R - k] + " = cf{" + A + ".x - " + B + ".y, " + A + ".y + " + B + ".x};");
