@@ -189,7 +189,12 @@ int fftc_jit_codelet_source(int R, char* buf, size_t len);
  * size, -4 compile error); the NVRTC log goes to log (may be NULL).        */
 int fftc_jit_compile(int64_t N, char* log, size_t loglen);
 
-/* Host only: compile the JIT pass kernel for pass length L (<= 256, prime factors <= 61;
+/* Host only: the generated CUDA source of the pass kernel for pass length L (the kernel
+ * fftc_jit_pass_compile compiles).  Returns its length, or -1 if L is not a JIT pass
+ * length.  Truncation and NUL termination as fftc_jit_source.             */
+int fftc_jit_pass_source(int L, char* buf, size_t len);
+
+/* Host only: compile the JIT pass kernel for pass length L (<= 512, prime factors <= 61;
  * the runtime multi-pass path above 4096 specialises each pass this way).  Returns the
  * cubin size, or < 0 as fftc_jit_compile.                                 */
 int fftc_jit_pass_compile(int L, char* log, size_t loglen);

@@ -78,6 +78,7 @@ def load(path: str = LIB_PATH):
         "fftc_plan_create_direct": ([i64, i64, i32], vp),
         "fftc_jit_compile": ([i64, ctypes.c_char_p, sz], i32),
         "fftc_jit_pass_compile": ([i32, ctypes.c_char_p, sz], i32),
+        "fftc_jit_pass_source": ([i32, ctypes.c_char_p, sz], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -190,6 +191,15 @@ def fftc_jit_compile(N: int):
     log = ctypes.create_string_buffer(1 << 16)
     r = load().fftc_jit_compile(N, log, 1 << 16)
     return r, log.value.decode(errors="replace")
+
+
+def fftc_jit_pass_source(L: int):
+    n = load().fftc_jit_pass_source(L, None, 0)
+    if n < 0:
+        return None
+    buf = ctypes.create_string_buffer(n + 1)
+    load().fftc_jit_pass_source(L, buf, n + 1)
+    return buf.value.decode()
 
 
 def fftc_jit_pass_compile(L: int):

@@ -766,6 +766,18 @@ int fftc_jit_compile(int64_t N, char* log, size_t loglen) {
   return rc == 0 ? (int)cubin.size() : rc;
 }
 
+int fftc_jit_pass_source(int L, char* buf, size_t len) {
+  int R[32];
+  const int S = jit_pass_radices(L, R, 32);
+  if (L < 2 || L > kJitPassMaxL || S < 1) return -1;
+  const std::string src = jit_pass_source(L, R, S);
+  if (buf && len) {
+    strncpy(buf, src.c_str(), len - 1);
+    buf[len - 1] = 0;
+  }
+  return (int)src.size();
+}
+
 int fftc_jit_pass_compile(int L, char* log, size_t loglen) {
   int R[32];
   const int S = jit_pass_radices(L, R, 32);

@@ -324,49 +324,6 @@ void emit_stages(std::string& s, int L, const int* R, int S, const char* count, 
   }
 }
 
-// In-place variant for long passes (one buffer, half the shared memory): every thread first
-// reads all of its butterflies of the stage into registers (KB = ceil(COLS NB / T) per thread,
-// compile-time), the CTA syncs, then writes -- as the compiled fused kernels do.
-void emit_stages_inplace(std::string& s, int L, const int* R, int S, int COLS, int T, int P) {
-  char b[900];
-  int Ns = 1;
-  for (int i = 0; i < S; ++i) {
-    const int Rs = R[i], NB = L / Rs, KB = (COLS * NB + T - 1) / T;
-    snprintf(b, sizeof b,
-             "  { // sub-stage %d (in place): radix %d, Ns %d\n"
-             "    cf v[%d][%d]; int jj[%d], ff[%d];\n"
-             "#pragma unroll\n"
-             "    for (int kb = 0; kb < %d; ++kb) { const int q = threadIdx.x + kb * T; ff[kb] = -1;\n"
-             "      if (q < nc * %d) { const int f = q / %d, j = q %% %d; ff[kb] = f; jj[kb] = j;\n"
-             "#pragma unroll\n"
-             "        for (int r = 0; r < %d; ++r) v[kb][r] = A[f * %d + j + r * %d]; } }\n"
-             "    __syncthreads();\n"
-             "#pragma unroll\n"
-             "    for (int kb = 0; kb < %d; ++kb) { if (ff[kb] < 0) continue; const int f = ff[kb], j = jj[kb], m = j %% %d;\n",
-             i, Rs, Ns, KB, Rs, KB, KB, KB, NB, NB, NB, Rs, P, NB, KB, Ns);
-    s += b;
-    if (Ns > 1) {
-      snprintf(b, sizeof b,
-               "#pragma unroll\n"
-               "      for (int r = 1; r < %d; ++r) { const cf w = tw[%d + (r - 1) * %d + m];\n"
-               "        v[kb][r] = cf{fmaf(v[kb][r].x, w.x, -v[kb][r].y * w.y), fmaf(v[kb][r].x, w.y, v[kb][r].y * w.x)}; }\n",
-               Rs, Ns - 1, Ns);
-      s += b;
-    }
-    snprintf(b, sizeof b,
-             "      dft%d(v[kb]);\n"
-             "      const int o = (j / %d) * %d + m;\n"
-             "#pragma unroll\n"
-             "      for (int r = 0; r < %d; ++r) A[f * %d + o + r * %d] = v[kb][r];\n"
-             "    }\n"
-             "    __syncthreads();\n"
-             "  }\n",
-             Rs, Ns, Ns * Rs, Rs, P, Ns);
-    s += b;
-    Ns *= Rs;
-  }
-}
-
 std::string prelude(const int* R, int S) {
   std::string s = "struct alignas(8) cf { float x, y; };\n";
   std::vector<int> done;
@@ -408,76 +365,245 @@ std::string jit_source(int N) {
   return s;
 }
 
+// Geometry of a JIT pass kernel: COLS adjacent columns per CTA held in shared memory as
+// [column][row] at an odd pitch LP (conflict-free both along rows and across columns), T threads.
+// Chosen so that every sub-stage's COLS*L/R butterflies split evenly over the threads (no idle
+// round), each thread's load/store column stays fixed (T a multiple of COLS), at most 48
+// complex values per thread in registers, <= 100 KB of shared memory (>= 2 CTAs per SM), and
+// the tile large enough to amortise the per-CTA work.
+PassGeo jit_pass_geo(int L, const int* R, int S) {
+  PassGeo best;  // cols == 0: no feasible geometry (callers report UNSUPPORTED_SIZE)
+  double bscore = -1.0;
+  const int lp = L | 1;
+  for (int cols = 8; cols <= 256; cols *= 2) {
+    const size_t smem = (size_t)cols * lp * 8;
+    if (smem > (size_t)100 * 1024) break;
+    for (int T = 64; T <= 512; T += 32) {
+      if (T % cols) continue;
+      const int rstep = T / cols, E = (L + rstep - 1) / rstep;
+      if (E > 64) continue;
+      double useful = 0.0, slots = 0.0;
+      int vals = E < kJitLoadRound ? E : kJitLoadRound;  // complex values live per thread
+      bool ok = true;
+      for (int q = 0; q < S; ++q) {
+        const int nb = cols * (L / R[q]), kb = (nb + T - 1) / T;
+        if (kb * R[q] > (R[q] > 32 ? R[q] : 32)) ok = false;  // one butterfly of a large prime is allowed
+        if (kb * R[q] > vals) vals = kb * R[q];
+        useful += (double)nb * R[q];
+        slots += (double)kb * T * R[q];
+      }
+      if (!ok) continue;
+      const double eff = (useful / slots) * ((double)L / ((double)E * rstep));
+      const double tile = (double)cols * L;
+      // resident CTAs per SM: registers (estimate: 2 per complex value + ~48 for addresses,
+      // twiddles and codelet temporaries) and shared memory; at least two so one CTA's loads
+      // and stores overlap another's compute
+      const int regs = 2 * vals + 48;
+      const int ctas_reg = 65536 / (T * (regs > 64 ? regs : 64));
+      const int ctas_smem = (int)((227 * 1024) / (smem + 1024));
+      const int ctas = ctas_reg < ctas_smem ? ctas_reg : ctas_smem;
+      if (ctas < 1) continue;
+      const double warps = (double)ctas * T / 32.0;
+      const double score = eff + 0.03 * (tile < 4096 ? tile / 4096 : 1.0) + 0.06 * (warps < 24 ? warps / 24 : 1.0) +
+                           (ctas >= 2 ? 0.1 : 0.0);
+      if (score > bscore + 1e-9) {
+        bscore = score;
+        best.cols = cols;
+        best.threads = T;
+        best.lp = lp;
+        best.minb = ctas >= 2 ? 2 : 1;  // __launch_bounds__ minimum CTAs per SM
+      }
+    }
+  }
+  return best;
+}
+
 int jit_pass_cols(int L) {
-  if (L > 256) return 8;  // long passes: in place, 8 columns (64-byte rows), <= 66 KB
-  int c = 16;
-  while (c < 256 && 2 * c * L <= 4096) c *= 2;
-  return c;
+  int R[32];
+  const int S = jit_pass_radices(L, R, 32);
+  return S > 0 ? jit_pass_geo(L, R, S).cols : 0;
 }
 size_t jit_pass_smem(int L) {
-  return (size_t)(L > 256 ? 1 : 2) * jit_pass_cols(L) * (L + 1) * 8;
+  int R[32];
+  const int S = jit_pass_radices(L, R, 32);
+  if (S <= 0) return 0;
+  const PassGeo g = jit_pass_geo(L, R, S);
+  return (size_t)g.cols * g.lp * 8;
 }
 
 // One pass of the runtime multi-pass path (the kernel of gpass.cu) with L, its radices and
-// the column count compiled in: straight-line codelets (any prime up to kJitMaxPrime),
-// constant-divisor index math.  Ns, the twiddle split and the sizes stay runtime arguments,
-// so one kernel serves every pass of that length.
-std::string jit_pass_source(int L, const int* R, int S) {
-  const int LP = L + 1, COLS = jit_pass_cols(L);
-  int LC = 0;
-  while ((1 << LC) < COLS) ++LC;
-  std::string s = "// generated by libfftc (jit.cpp): pass of length " + std::to_string(L) + "\n" + prelude(R, S);
-  char b[900];
-  snprintf(b, sizeof b,
-           "extern \"C\" __global__ void __launch_bounds__(%d, 4) fftc_jit_pass(const cf* __restrict__ in,\n"
-           "    cf* __restrict__ out, const cf* __restrict__ tw, const cf* __restrict__ twA, const cf* __restrict__ twB,\n"
-           "    long long N, int Ns, int tws, int tiles, float csign_in, float csign_out) {\n"
-           "  extern __shared__ cf sm[];\n"
-           "  constexpr int L = %d, LP = %d, COLS = %d, LC = %d, T = %d;\n"
-           "  __shared__ int s_cq[COLS], s_cm[COLS];\n",
-           kJitThreads, L, LP, COLS, LC, kJitThreads);
-  s += b;
-  s += "  const long long NB = N / L;\n"
-       "  const long long bt = blockIdx.x / tiles;\n"
-       "  const long long c0 = (long long)(blockIdx.x % tiles) * COLS;\n"
-       "  const int nc = (int)(NB - c0 < COLS ? NB - c0 : COLS);\n"
-       "  cf* A = sm;\n"
-       "  for (int f = threadIdx.x; f < COLS; f += T) { const int c = (int)c0 + f; s_cq[f] = c / Ns; s_cm[f] = c - (c / Ns) * Ns; }\n"
-       "  __syncthreads();\n"
-       "  const cf* gi = in + bt * N + c0;\n"
-       "  const long long amask = (1LL << tws) - 1;\n"
-       "  for (int e0 = threadIdx.x; e0 < (L << LC); e0 += 8 * T) {\n"
-       "    cf v[8];\n"
-       "#pragma unroll\n"
-       "    for (int u = 0; u < 8; ++u) { const int e = e0 + u * T, f = e & (COLS - 1), r = e >> LC;\n"
-       "      v[u] = (e < (L << LC) && f < nc) ? gi[f + (long long)r * NB] : cf{0.f, 0.f}; }\n"
-       "#pragma unroll\n"
-       "    for (int u = 0; u < 8; ++u) { const int e = e0 + u * T, f = e & (COLS - 1), r = e >> LC;\n"
-       "      if (e < (L << LC) && f < nc) { cf x = v[u]; x.y *= csign_in;\n"
-       "        if (Ns > 1) { const long long ex = (long long)s_cm[f] * r;\n"
-       "          const cf p = twA[ex & amask], q = twB[ex >> tws];\n"
-       "          const cf w = cf{fmaf(p.x, q.x, -p.y * q.y), fmaf(p.x, q.y, p.y * q.x)};\n"
-       "          x = cf{fmaf(x.x, w.x, -x.y * w.y), fmaf(x.x, w.y, x.y * w.x)}; }\n"
-       "        A[f * LP + r] = x; } }\n"
-       "  }\n"
-       "  __syncthreads();\n";
-  if (L > 256) {
-    emit_stages_inplace(s, L, R, S, COLS, kJitThreads, LP);
-  } else {
-    s += "  cf* B = sm + COLS * LP;\n";
-    emit_stages(s, L, R, S, "nc", LP);
+// the tile geometry compiled in: straight-line codelets (any prime up to kJitMaxPrime), every
+// loop trip count and divisor a compile-time constant.  Ns, the twiddle split and the sizes
+// stay runtime arguments, so one kernel serves every pass of that length.  Pass s is one level
+// of Eq. 2 at the pass level: column c reads a[c + r NB], multiplies by
+// w_{Ns L}^{(c mod Ns) r}, runs DFT_L as in-place Stockham sub-stages, writes the autosort
+// position (c div Ns) Ns L + (c mod Ns) + r Ns.  Each thread loads and stores ONE column f
+// (rows r = rs + u RSTEP), so its twiddles are w^{m rs} times powers of w^{m RSTEP} (a tree:
+// powers 2^b looked up once per thread, every other one a single product).
+namespace {
+// replace every "$NAME" in t by its value
+std::string subst(std::string t, const std::vector<std::pair<std::string, std::string>>& kv) {
+  for (const auto& p : kv) {
+    const std::string key = "$" + p.first;
+    for (size_t at = t.find(key); at != std::string::npos; at = t.find(key, at + p.second.size()))
+      t.replace(at, key.size(), p.second);
   }
-  s += "  cf* go = out + bt * N;\n"
-       "  if (Ns == 1) {\n"
-       "    for (int e = threadIdx.x; e < nc * L; e += T) { const int f = e / L, r = e - (e / L) * L;\n"
-       "      const cf a = A[f * LP + r]; go[(c0 + f) * L + r] = cf{a.x, csign_out * a.y}; }\n"
-       "  } else {\n"
-       "    for (int e = threadIdx.x; e < (L << LC); e += T) { const int f = e & (COLS - 1), r = e >> LC;\n"
-       "      if (f < nc) { const cf a = A[f * LP + r];\n"
-       "        go[((long long)s_cq[f] * L + r) * Ns + s_cm[f]] = cf{a.x, csign_out * a.y}; } }\n"
-       "  }\n"
-       "}\n";
-  return s;
+  return t;
+}
+}  // namespace
+
+std::string jit_pass_source(int L, const int* R, int S) {
+  const PassGeo g = jit_pass_geo(L, R, S);
+  if (g.cols <= 0) return "";
+  const int COLS = g.cols, T = g.threads, RSTEP = T / COLS, E = (L + RSTEP - 1) / RSTEP;
+  const int UR = E < kJitLoadRound ? E : kJitLoadRound;
+  std::string s = "// generated by libfftc (jit.cpp): pass of length " + std::to_string(L) + "\n" + prelude(R, S);
+  // the body is a template on FIRST (pass 0: Ns = 1, no input twiddle, contiguous column
+  // outputs); fftc_jit_pass_first / fftc_jit_pass instantiate it, so neither carries the other's
+  // code under a runtime predicate
+  s += R"(template <bool FIRST, bool CI, bool CO>
+__device__ __forceinline__ void pass_body(const cf* __restrict__ in, cf* __restrict__ out, const cf* __restrict__ tw,
+    const cf* __restrict__ twA, const cf* __restrict__ twB, long long N, int Ns, int tws, int tiles, float csign_in,
+    float csign_out) {
+  extern __shared__ cf A[];
+  constexpr int L = $L, LP = $LP, COLS = $COLS, T = $T, RSTEP = $RSTEP, E = $E, UR = $UR;
+  const int NB = (int)(N / L);  // columns of this pass (< 2^31)
+  const int bt = (int)(blockIdx.x / tiles);
+  const int c0 = (int)(blockIdx.x - bt * tiles) * COLS;
+  const int nc = NB - c0 < COLS ? NB - c0 : COLS;
+  const int f = threadIdx.x % COLS, rs = threadIdx.x / COLS;  // this thread's column and first row
+  const int c = c0 + f, cq = c / Ns, cm = c - cq * Ns;
+  const bool fok = f < nc;
+  const long long amask = (1LL << tws) - 1;
+  auto root = [&](long long e) { const cf p = twA[e & amask], q = twB[e >> tws];
+    return cf{fmaf(p.x, q.x, -p.y * q.y), fmaf(p.x, q.y, p.y * q.x)}; };
+  auto cmulf = [](cf a, cf w) { return cf{fmaf(a.x, w.x, -a.y * w.y), fmaf(a.x, w.y, a.y * w.x)}; };
+  {  // column f, rows r_u = rs + u RSTEP: loaded in rounds of UR (a round's loads all in flight)
+    const cf* gp = in + (long long)bt * N + c + (long long)rs * NB;
+    const long long gstep = (long long)RSTEP * NB;
+    // input twiddle w^{m r_u}, m = c mod Ns: looked up for u = 0 mod 8, else that times
+    // st[u mod 8] = w^{m (u mod 8) RSTEP} -- one lookup, the other powers as products (a tree:
+    // st[k] = st[2^b] st[k - 2^b], at most three products deep)
+    cf st[8];
+    if (!FIRST) {
+      st[1] = root((long long)cm * RSTEP);
+#pragma unroll
+      for (int k = 2; k < (E < 8 ? E : 8); ++k) {
+        const int hb = k >= 4 ? 4 : 2;
+        st[k] = k == hb ? cmulf(st[hb / 2], st[hb / 2]) : cmulf(st[hb], st[k - hb]);
+      }
+    }
+#pragma unroll
+    for (int u0 = 0; u0 < E; u0 += UR) {
+      cf v[UR];
+#pragma unroll
+      for (int k = 0; k < UR; ++k) {
+        const int u = u0 + k;
+        if (u < E && (L % RSTEP == 0 || rs + u * RSTEP < L)) v[k] = fok ? gp[u * gstep] : cf{0.f, 0.f};
+      }
+      cf base = cf{1.f, 0.f};
+#pragma unroll
+      for (int k = 0; k < UR; ++k) {
+        const int u = u0 + k, r = rs + u * RSTEP;
+        if (u < E && (L % RSTEP == 0 || r < L)) {
+          cf x = v[k];
+          if (CI) x.y = -x.y;
+          if (!FIRST) {
+            if ((u & 7) == 0 || k == 0) base = root((long long)cm * (rs + (u & ~7) * RSTEP));
+            x = (u & 7) ? cmulf(x, cmulf(base, st[u & 7])) : cmulf(x, base);
+          }
+          A[f * LP + r] = x;  // columns >= nc carry zeros: computed, never stored to HBM
+        }
+      }
+    }
+  }
+  __syncthreads();
+)";
+  // in-place sub-stages: KB butterfly rounds per thread, all read before the barrier, then written
+  int Ns = 1;
+  for (int i = 0; i < S; ++i) {
+    const int Rs = R[i], NB = L / Rs, KB = (COLS * NB + T - 1) / T;
+    const bool exact = (COLS * NB) % T == 0;
+    std::string st = R"(  {  // sub-stage $I: radix $R, Ns $NS, $KB butterfly round(s) per thread
+    cf v[$KB][$R];
+#pragma unroll
+    for (int kb = 0; kb < $KB; ++kb) {
+      const int q = threadIdx.x + kb * T, ff = q / $NB, j = q - ff * $NB;
+      if ($GUARD) {
+#pragma unroll
+        for (int r = 0; r < $R; ++r) v[kb][r] = A[ff * LP + j + r * $NB];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kb = 0; kb < $KB; ++kb) {
+      const int q = threadIdx.x + kb * T, ff = q / $NB, j = q - ff * $NB;
+      if ($GUARD) {
+        const int m = j % $NS;
+$TW        dft$R(v[kb]);
+        const int o = (j / $NS) * $NSR + m;
+#pragma unroll
+        for (int r = 0; r < $R; ++r) A[ff * LP + o + r * $NS] = v[kb][r];
+      }
+    }
+    __syncthreads();
+  }
+)";
+    const std::string tws = Ns > 1 ? "#pragma unroll\n        for (int r = 1; r < " + std::to_string(Rs) +
+                                          "; ++r) v[kb][r] = cmulf(v[kb][r], tw[" + std::to_string(Ns - 1) +
+                                          " + (r - 1) * " + std::to_string(Ns) + " + m]);\n"
+                                    : "";
+    s += subst(st, {{"I", std::to_string(i)},
+                    {"KB", std::to_string(KB)},
+                    {"NSR", std::to_string(Ns * Rs)},
+                    {"NS", std::to_string(Ns)},
+                    {"NB", std::to_string(NB)},
+                    {"GUARD", exact ? "true" : "q < COLS * " + std::to_string(NB)},
+                    {"TW", tws},
+                    {"R", std::to_string(Rs)}});
+    Ns *= Rs;
+  }
+  s += R"(  cf* go = out + (long long)bt * N;
+  if (FIRST) {  // first pass: column c's L outputs are contiguous at c L + r (lanes walk them)
+    cf* gout = go + (long long)c0 * L;
+#pragma unroll 4
+    for (int e = threadIdx.x; e < COLS * L; e += T) {
+      const int ff = e / L, r = e - ff * L;
+      if (ff < nc) { const cf a = A[ff * LP + r]; gout[e] = cf{a.x, CO ? -a.y : a.y}; }
+    }
+  } else if (fok) {  // autosort position (c div Ns) Ns L + (c mod Ns) + r Ns (lanes walk c)
+    cf* gs = go + (long long)cq * Ns * L + cm + (long long)rs * Ns;
+    const long long sstep = (long long)RSTEP * Ns;
+#pragma unroll
+    for (int u = 0; u < E; ++u) {
+      const int r = rs + u * RSTEP;
+      if (L % RSTEP == 0 || r < L) { const cf a = A[f * LP + r]; gs[u * sstep] = cf{a.x, CO ? -a.y : a.y}; }
+    }
+  }
+}
+#define FFTC_PASS_ARGS const cf* __restrict__ in, cf* __restrict__ out, const cf* __restrict__ tw, \
+    const cf* __restrict__ twA, const cf* __restrict__ twB, long long N, int Ns, int tws, int tiles, float csign_in, \
+    float csign_out
+// entry points: first pass or not x conjugated input (inverse, first pass) x conjugated output
+// (inverse, last pass); the sign multiplies are compiled in, not applied at run time
+#define FFTC_PASS_ENTRY(NAME, FIRST, CI, CO) \
+  extern "C" __global__ void __launch_bounds__($T, $MINB) NAME(FFTC_PASS_ARGS) { \
+    pass_body<FIRST, CI, CO>(in, out, tw, twA, twB, N, Ns, tws, tiles, csign_in, csign_out); }
+FFTC_PASS_ENTRY(fftc_jit_pass, false, false, false)
+FFTC_PASS_ENTRY(fftc_jit_pass_co, false, false, true)
+FFTC_PASS_ENTRY(fftc_jit_pass_first, true, false, false)
+FFTC_PASS_ENTRY(fftc_jit_pass_first_ci, true, true, false)
+FFTC_PASS_ENTRY(fftc_jit_pass_first_cico, true, true, true)
+FFTC_PASS_ENTRY(fftc_jit_pass_first_co, true, false, true)
+)";
+  return subst(s, {{"MINB", std::to_string(g.minb)},
+                   {"COLS", std::to_string(COLS)},
+                   {"RSTEP", std::to_string(RSTEP)},
+                   {"LP", std::to_string(g.lp)},
+                   {"UR", std::to_string(UR)},
+                   {"T", std::to_string(T)},
+                   {"L", std::to_string(L)},
+                   {"E", std::to_string(E)}});
 }
 
 // ---------------------------------------------------------------- NVRTC + driver API
@@ -561,7 +687,8 @@ int compile_src(const std::string& src, std::string* cubin, std::string* log) {
 
 // Compile + load `src`, kernel `name`, dynamic shared memory `smem`; cached under `key`.
 const JitKernel* load_kernel(const std::string& key, const std::string& src, const char* name, size_t smem, int N,
-                             int fpb, cudaError_t* err) {
+                             int fpb, cudaError_t* err, const char* const* more = nullptr, int nmore = 0,
+                             int threads = kJitThreads) {
   std::lock_guard<std::mutex> lk(g_mu);
   // a loaded CUfunction belongs to the context (device) it was loaded in: cache per device
   int dev = 0;
@@ -597,7 +724,12 @@ const JitKernel* load_kernel(const std::string& key, const std::string& src, con
   k->N = N;
   k->fpb = fpb;
   k->smem = smem;
-  if (setattr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)k->smem) != CUDA_SUCCESS) {
+  k->threads = threads;
+  bool ok = setattr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)k->smem) == CUDA_SUCCESS;
+  for (int i = 0; i < nmore && i < JitKernel::kVariants && ok; ++i)
+    ok = getfn(&k->variant[i], mod, more[i]) == CUDA_SUCCESS &&
+         setattr(k->variant[i], CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)k->smem) == CUDA_SUCCESS;
+  if (!ok) {
     delete k;
     *err = cudaErrorInvalidValue;
     return nullptr;
@@ -625,8 +757,18 @@ const JitKernel* jit_get(int N, cudaError_t* err) {
 const JitKernel* jit_pass_get(int L, const int* R, int S, cudaError_t* err) {
   std::string key = "p:" + std::to_string(L);
   for (int i = 0; i < S; ++i) key += ":" + std::to_string(R[i]);
-  const int cols = jit_pass_cols(L);
-  return load_kernel(key, jit_pass_source(L, R, S), "fftc_jit_pass", jit_pass_smem(L), L, cols, err);
+  const PassGeo g = jit_pass_geo(L, R, S);
+  if (g.cols <= 0) {
+    *err = cudaErrorNotSupported;
+    return nullptr;
+  }
+  // variant[first * 4 + ci * 2 + co], the combinations a plan uses (the first pass never has
+  // co without being the last, but all six entry points exist)
+  static const char* const names[JitKernel::kVariants] = {
+      "fftc_jit_pass", "fftc_jit_pass_co", "fftc_jit_pass", "fftc_jit_pass_co",
+      "fftc_jit_pass_first", "fftc_jit_pass_first_co", "fftc_jit_pass_first_ci", "fftc_jit_pass_first_cico"};
+  return load_kernel(key, jit_pass_source(L, R, S), "fftc_jit_pass", (size_t)g.cols * g.lp * 8, L, g.cols, err,
+                     names, JitKernel::kVariants, g.threads);
 }
 
 cudaError_t jit_pass_launch(const JitKernel* k, const float2* in, float2* out, const float2* tw, const float2* twA,
@@ -644,8 +786,10 @@ cudaError_t jit_pass_launch(const JitKernel* k, const float2* in, float2* out, c
   float ci = conj_in ? -1.f : 1.f, co = conj_out ? -1.f : 1.f;
   void* args[] = {(void*)&in, (void*)&out, (void*)&tw, (void*)&twA, (void*)&twB, (void*)&N, (void*)&Ns,
                   (void*)&tws, (void*)&tiles, (void*)&ci, (void*)&co};
-  const CUresult r = launch(k->fn, (unsigned)grid, 1, 1, kJitThreads, 1, 1, (unsigned)k->smem, (CUstream)st, args,
-                            nullptr);
+  // Ns = 1 only for the first pass; conj_in is set only there (the inverse's input conjugation)
+  CUfunction fn = k->variant[(Ns == 1 ? 4 : 0) + (conj_in ? 2 : 0) + (conj_out ? 1 : 0)];
+  const CUresult r = launch(fn, (unsigned)grid, 1, 1, (unsigned)k->threads, 1, 1, (unsigned)k->smem, (CUstream)st,
+                            args, nullptr);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorLaunchFailure;
 }
 

@@ -10,13 +10,25 @@ namespace fftc {
 
 constexpr int kJitMaxPrime = 61;  // largest prime radix the JIT emits (conjugate-pair form, O(p^2))
 constexpr int kJitThreads = 256;
-constexpr int kJitTile = 4096;    // elements per CTA (FPB = 4096 / N transforms)
+constexpr int kJitTile = 4096;
+constexpr int kJitLoadRound = 16;  // JIT pass kernels: rows loaded per thread per round    // elements per CTA (FPB = 4096 / N transforms)
 
 struct JitKernel {
   CUfunction fn;
+  // pass kernels: entry point per (first pass, conjugated input, conjugated output), index
+  // first * 4 + ci * 2 + co (jit_pass_launch)
+  static constexpr int kVariants = 8;
+  CUfunction variant[kVariants] = {};
   int N, fpb;
   size_t smem;
+  int threads = kJitThreads;  // CTA size (pass kernels choose theirs, jit_pass_geo)
 };
+
+// Tile geometry of a JIT pass kernel of length L (jit.cpp): columns per CTA, threads, pitch.
+struct PassGeo {
+  int cols = 0, threads = 0, lp = 0, minb = 1;
+};
+PassGeo jit_pass_geo(int L, const int* R, int S);
 
 // Radix schedule for the JIT kernel (16/8/4/2, 9/3, 25/5, 7, then primes 11..kJitMaxPrime),
 // or -1 if N has a prime factor > kJitMaxPrime.
