@@ -27,7 +27,8 @@ roofline: the dominant kernel (the fused Stockham kernel for C2/C3; the pass ker
 c3 / c4: compact sub-records (N = 1) timing the mixed-radix and large-N configs beside
          the headline, each job's fraction of its §8(d) bound.
 c5:    (N > 1) the distributed six-step N = 2^30 over the N ranks (NCCL all-to-alls; fused
-         peer-store exchanges; fused + transposed output), under a watchdog.
+         peer-store exchanges; fused + transposed output), run as its own torchrun job so a
+         crash or hang there cannot cost the headline line.
 cpu_baseline: the oracle's recursive Cooley-Tukey (oracle/, fp64, OpenMP) on a bounded
          sample of the same workload (rank 0, N = 1 only).
 """
@@ -201,7 +202,10 @@ class Dist:
         torch.cuda.set_device(self.local)
         if self.world > 1:
             import torch.distributed as dist
-            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            import datetime
+            # long timeout: ranks != 0 wait at a barrier while rank 0 runs the c5 child job
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local),
+                                    timeout=datetime.timedelta(minutes=30))
             self.pg = dist
 
     def barrier(self):
@@ -397,46 +401,31 @@ def sub_record(workload, dev, K, W, peak):
             "ncu_source": src, "jobs": recs}
 
 
-def c5_sub_record(D, dev, steps, warm, timeout_s, line_holder):
-    """Six-step N = 2^30 over the ranks: default NCCL exchanges, fused peer stores, fused +
-    transposed output.  Rank r's slab is elements [r N/P, (r+1) N/P) of the one seeded vector."""
-    import torch
-    import synth
-    import paper_2207_06803_b200 as fftc
-    N = 1 << 30
-    P = D.world
-    slab = N // P
-    x = torch.from_numpy(synth.uniform_c64_rows(1, D.rank * slab, (D.rank + 1) * slab, seed=0).reshape(-1)).to(dev)
-    y = torch.empty_like(x)
-    stream = torch.cuda.current_stream(dev)
-    res = {"N": N, "ranks": P, "nvlink_bytes_per_rank_per_a2a": (P - 1) / P * 8 * N / P, "variants": []}
-    for flags, name in ((0, "nccl a2a x3"), (2, "fused peer stores"), (3, "fused peer stores + transposed out")):
-        idt = torch.zeros(fftc.FFTC_NCCL_ID_BYTES, dtype=torch.uint8, device=dev)
-        if D.rank == 0:
-            idt.copy_(torch.frombuffer(bytearray(fftc.fftc_dist_get_unique_id()), dtype=torch.uint8))
-        D.pg.broadcast(idt, 0)
-        plan = fftc.Plan.dist(N, -1, bytes(idt.cpu().numpy().tobytes()), D.rank, P, flags=flags)
-        for _ in range(warm):
-            plan.execute(x, y)
-        torch.cuda.synchronize(dev)
-        D.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(steps):
-            plan.execute(x, y)
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        t = D.max([e0.elapsed_time(e1) / 1e3])[0] / steps
-        na2a = 2 if flags & 1 else 3
-        res["variants"].append({"flags": flags, "exchange": name, "ms": round(t * 1e3, 3),
-                                "gflops": round(flops(N, 1) / t / 1e9, 1),
-                                "a2a_per_step": na2a,
-                                "nvlink_GBs_per_rank_lower_bound": round(
-                                    na2a * res["nvlink_bytes_per_rank_per_a2a"] / t / 1e9, 1),
-                                "plan": plan.describe()})
-        plan.close()
-        line_holder["c5"] = res
-    return res
+def c5_child(args, world):
+    """The distributed six-step at N = 2^30 over `world` ranks, run as a SEPARATE torchrun job
+    (rank 0 of the headline run launches it and waits, the other ranks wait at a barrier), so a
+    crash or hang in the NCCL / CUDA-IPC exchanges -- code that has not run on real NVLink yet --
+    cannot cost the headline line.  Returns the child's JSON record or {"error": ...}."""
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "LOCAL_WORLD_SIZE", "GROUP_RANK", "ROLE_RANK",
+                        "ROLE_WORLD_SIZE", "GROUP_WORLD_SIZE", "MASTER_ADDR", "MASTER_PORT")
+           and not k.startswith("TORCHELASTIC")}
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(world),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__),
+           "--gpus", str(world), "--workload", "c5", "--steps", "5", "--warmup", "2", "--c5-variants", "0,2,3"]
+    try:
+        r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=args.c5_timeout)
+    except subprocess.TimeoutExpired:
+        return {"error": "six-step child job not finished after %d s" % args.c5_timeout}
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    if r.returncode != 0 or not lines:
+        return {"error": "six-step child job rc=%d: %s" % (r.returncode, (r.stderr or r.stdout)[-400:])}
+    d = json.loads(lines[-1])
+    return {k: d[k] for k in ("value", "unit", "ms_per_step", "n_gpus", "variants", "config") if k in d}
 
 
 def run_fftc(args):
@@ -497,7 +486,6 @@ def run_fftc(args):
         topo = {"comm_nranks_ok": len(uuids) == args.gpus, "gpus_active": len(set(uuids))}
 
     line_holder = {}
-    extras_done = threading.Event()
     if D.world == 1 and args.workload == "c2" and not args.no_extras:
         js.close()
         js.dbufs, js.outs = {}, []
@@ -543,23 +531,14 @@ def run_fftc(args):
         print(json.dumps(line), flush=True)
 
     if D.world > 1 and args.workload == "c2" and not args.no_extras:
-        # the six-step over NCCL / NVLink; a hang here must not cost the headline line
-        def on_timeout():
-            if not extras_done.is_set():
-                line_holder.setdefault("c5", {})["error"] = "watchdog: not finished after %d s" % args.c5_timeout
-                emit()
-                os._exit(0)
-        wd = threading.Timer(args.c5_timeout, on_timeout)
-        wd.daemon = True
-        wd.start()
+        # the six-step over NCCL / NVLink in its own job (c5_child); the ranks of this job free
+        # their buffers and wait
         js.close()
+        js.dbufs, js.outs = {}, []
         torch.cuda.empty_cache()
-        try:
-            c5_sub_record(D, dev, 5, 2, args.c5_timeout, line_holder)
-        except Exception as e:
-            line_holder.setdefault("c5", {})["error"] = "%s: %s" % (type(e).__name__, e)
-        extras_done.set()
-        wd.cancel()
+        if D.rank == 0:
+            line_holder["c5"] = c5_child(args, D.world)
+        D.barrier()
     emit()
     js.close()
     D.close()
@@ -634,6 +613,8 @@ def run_c5(args):
     else:
         nid = None
     lb = args.c5_loopback if D.world == 1 else 0
+    if args.c5_variants:
+        return run_c5_variants(args, D, dev, N)
     plan = fftc.Plan.dist(N, -1, nid, D.rank, lb or D.world, loopback=bool(lb), flags=args.c5_flags)
     slab = N // D.world
     # rank r holds elements [r N/P, (r+1) N/P) of the one seeded U[-1,1) vector
@@ -671,6 +652,51 @@ def run_c5(args):
                 "gpu_launches": plan.launches() * K, "clocks": sampler.summary()}
         print(json.dumps(line), flush=True)
     plan.close()
+    D.close()
+
+
+def run_c5_variants(args, D, dev, N):
+    """Six-step over the ranks for each exchange mode in --c5-variants (0: NCCL all-to-alls,
+    2: fused peer stores, 3: fused + transposed output); one line with every variant's time."""
+    import torch
+    import synth
+    import paper_2207_06803_b200 as fftc
+    P = D.world
+    slab = N // P
+    x = torch.from_numpy(synth.uniform_c64_rows(1, D.rank * slab, (D.rank + 1) * slab, seed=0).reshape(-1)).to(dev)
+    y = torch.empty_like(x)
+    stream = torch.cuda.current_stream(dev)
+    a2a = (P - 1) / P * 8 * N / P
+    names = {0: "nccl a2a x3", 1: "nccl, transposed out", 2: "fused peer stores", 3: "fused peer stores + transposed out"}
+    out = []
+    for flags in [int(v) for v in args.c5_variants.split(",")]:
+        idt = torch.zeros(fftc.FFTC_NCCL_ID_BYTES, dtype=torch.uint8, device=dev)
+        if D.rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(fftc.fftc_dist_get_unique_id()), dtype=torch.uint8))
+        D.pg.broadcast(idt, 0)
+        plan = fftc.Plan.dist(N, -1, bytes(idt.cpu().numpy().tobytes()), D.rank, P, flags=flags)
+        for _ in range(args.warmup):
+            plan.execute(x, y)
+        torch.cuda.synchronize(dev)
+        D.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            plan.execute(x, y)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        t = D.max([e0.elapsed_time(e1) / 1e3])[0] / args.steps
+        na2a = 2 if flags & 1 else 3
+        out.append({"flags": flags, "exchange": names.get(flags, str(flags)), "ms": round(t * 1e3, 3),
+                    "gflops": round(flops(N, 1) / t / 1e9, 1), "a2a_per_step": na2a,
+                    "nvlink_bytes_per_rank_per_a2a": a2a,
+                    "nvlink_GBs_per_rank_lower_bound": round(na2a * a2a / t / 1e9, 1), "plan": plan.describe()})
+        plan.close()
+    if D.rank == 0:
+        best = min(out, key=lambda v: v["ms"])
+        print(json.dumps({"metric": METRIC, "value": best["gflops"], "unit": UNIT, "n_gpus": P,
+                          "ms_per_step": best["ms"], "variants": out,
+                          "config": {"workload": "C5 six-step N=%d over %d ranks" % (N, P)}}), flush=True)
     D.close()
 
 
@@ -725,7 +751,8 @@ def main():
                     help="one GPU: run the six-step for P virtual ranks (all-to-alls = device copies)")
     ap.add_argument("--c5-flags", type=int, default=0,
                     help="six-step options: 1 = transposed output (no all-to-all #3), 2 = fused peer-store exchanges")
-    ap.add_argument("--c5-timeout", type=int, default=240, help="watchdog of the c5 sub-record (N > 1)")
+    ap.add_argument("--c5-timeout", type=int, default=300, help="time limit of the c5 sub-record's job (N > 1)")
+    ap.add_argument("--c5-variants", default="", help="--workload c5: time these exchange modes, e.g. 0,2,3")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the c3/c4 (N = 1) or c5 (N > 1) sub-records")
     ap.add_argument("--graph", action="store_true", help="also time the step captured in a CUDA graph")
