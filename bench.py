@@ -199,13 +199,18 @@ class Dist:
 
     def init(self):
         import torch
+        # FFTC_BENCH_BACKEND=gloo (test only): several ranks may then share one GPU to exercise
+        # the multi-rank logic on a one-GPU box (ranks never wait on one another's kernels)
+        backend = os.environ.get("FFTC_BENCH_BACKEND", "nccl")
+        if backend != "nccl":
+            self.local = self.local % torch.cuda.device_count()
         torch.cuda.set_device(self.local)
         if self.world > 1:
             import torch.distributed as dist
             import datetime
             # long timeout: ranks != 0 wait at a barrier while rank 0 runs the c5 child job
-            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local),
-                                    timeout=datetime.timedelta(minutes=30))
+            kw = {"device_id": torch.device("cuda", self.local)} if backend == "nccl" else {}
+            dist.init_process_group(backend, timeout=datetime.timedelta(minutes=30), **kw)
             self.pg = dist
 
     def barrier(self):
@@ -217,7 +222,8 @@ class Dist:
         if not self.pg:
             return list(values)
         import torch
-        t = torch.tensor(list(values), dtype=torch.float64, device="cuda")
+        nccl = os.environ.get("FFTC_BENCH_BACKEND", "nccl") == "nccl"
+        t = torch.tensor(list(values), dtype=torch.float64, device="cuda" if nccl else "cpu")
         self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
         return t.tolist()
 
