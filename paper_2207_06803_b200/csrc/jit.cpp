@@ -206,49 +206,6 @@ std::string codelet_fn(int R) {
 
 std::string jit_codelet_source(int R) { return (R >= 2 && R <= 128) ? codelet_fn(R) : std::string(); }
 
-int jit_radices(int N, int* R, int max) {
-  if (N < 2) return -1;
-  std::vector<int> out;
-  int n = N;
-  int a = 0;
-  while (n % 2 == 0) {
-    n /= 2;
-    ++a;
-  }
-  for (int i = 0; i < a / 4; ++i) out.push_back(16);
-  if (a % 4) out.push_back(1 << (a % 4));
-  while (n % 9 == 0) {
-    out.push_back(9);
-    n /= 9;
-  }
-  if (n % 3 == 0) {
-    out.push_back(3);
-    n /= 3;
-  }
-  while (n % 25 == 0) {
-    out.push_back(25);
-    n /= 25;
-  }
-  if (n % 5 == 0) {
-    out.push_back(5);
-    n /= 5;
-  }
-  while (n % 7 == 0) {
-    out.push_back(7);
-    n /= 7;
-  }
-  for (int p = 11; n > 1; p += 2) {
-    if (p > kJitMaxPrime) return -1;
-    while (n % p == 0) {
-      out.push_back(p);
-      n /= p;
-    }
-  }
-  if ((int)out.size() > max) return -1;
-  for (size_t i = 0; i < out.size(); ++i) R[i] = out[i];
-  return (int)out.size();
-}
-
 int jit_pass_radices(int L, int* R, int max) {
   std::vector<int> f;
   int n = L;
@@ -280,49 +237,26 @@ int jit_pass_radices(int L, int* R, int max) {
   return -1;
 }
 
-int jit_fpb(int N) {
-  int f = kJitTile / N;
-  return f < 1 ? 1 : f;
+int jit_radices(int N, int* R, int max) {
+  // the single-pass JIT kernel uses the pass kernels' balanced grouping (fewest stages with
+  // every radix <= 32 or a lone prime: fewer barriers and less unrolled code than peeling
+  // 16s, 9s, 25s and single primes off one at a time)
+  if (N < 2) return -1;
+  const int S = jit_pass_radices(N, R, max);
+  // smallest radix as the leaf (measured on B200 with the generated kernel: 143 as 11 x 13
+  // 0.26 ms vs 13 x 11 0.33 ms per 2^26 elements)
+  for (int a = 1; a < S; ++a)
+    for (int b = a; b > 0 && R[b] < R[b - 1]; --b) {
+      const int t = R[b];
+      R[b] = R[b - 1];
+      R[b - 1] = t;
+    }
+  return S;
 }
+
+
 
 namespace {
-
-// Stockham sub-stages of DFT_L over `count` rows (transforms / columns) held at pitch P in
-// shared memory, ping-ponging between A and B (one level of Eq. 2 per stage); twiddles from
-// the stage table `tw` (entry (Ns-1) + (r-1) Ns + m = w^{m r}).
-void emit_stages(std::string& s, int L, const int* R, int S, const char* count, int P) {
-  char b[640];
-  int Ns = 1;
-  for (int i = 0; i < S; ++i) {
-    const int Rs = R[i], NB = L / Rs;
-    snprintf(b, sizeof b,
-             "  { // sub-stage %d: radix %d, Ns %d\n"
-             "    for (int q = threadIdx.x; q < (%s) * %d; q += T) {\n"
-             "      const int f = q / %d, j = q %% %d, m = j %% %d;\n"
-             "      const cf* a = A + f * %d; cf* bb = B + f * %d;\n"
-             "      cf v[%d];\n"
-             "      for (int r = 0; r < %d; ++r) v[r] = a[j + r * %d];\n",
-             i, Rs, Ns, count, NB, NB, NB, Ns, P, P, Rs, Rs, NB);
-    s += b;
-    if (Ns > 1) {
-      snprintf(b, sizeof b,
-               "      for (int r = 1; r < %d; ++r) { const cf w = tw[%d + (r - 1) * %d + m];\n"
-               "        v[r] = cf{fmaf(v[r].x, w.x, -v[r].y * w.y), fmaf(v[r].x, w.y, v[r].y * w.x)}; }\n",
-               Rs, Ns - 1, Ns);
-      s += b;
-    }
-    snprintf(b, sizeof b,
-             "      dft%d(v);\n"
-             "      const int o = (j / %d) * %d + m;\n"
-             "      for (int r = 0; r < %d; ++r) bb[o + r * %d] = v[r];\n"
-             "    }\n"
-             "    __syncthreads(); cf* t = A; A = B; B = t;\n"
-             "  }\n",
-             Rs, Ns, Ns * Rs, Rs, Ns);
-    s += b;
-    Ns *= Rs;
-  }
-}
 
 std::string prelude(const int* R, int S) {
   std::string s = "struct alignas(8) cf { float x, y; };\n";
@@ -339,31 +273,17 @@ std::string prelude(const int* R, int S) {
 
 }  // namespace
 
-std::string jit_source(int N) {
-  int R[32];
-  const int S = jit_radices(N, R, 32);
-  if (S < 0) return "";
-  const int FPB = jit_fpb(N), NP = N | 1;
-  std::string s = "// generated by libfftc (jit.cpp) for N = " + std::to_string(N) + "\n" + prelude(R, S);
-  char b[512];
-  snprintf(b, sizeof b,
-           "extern \"C\" __global__ void __launch_bounds__(%d) fftc_jit(const cf* __restrict__ in, cf* __restrict__ out,\n"
-           "    const cf* __restrict__ tw, long long batch, float csign) {\n"
-           "  extern __shared__ cf sm[];\n"
-           "  constexpr int N = %d, FPB = %d, NP = %d, T = %d;\n",
-           kJitThreads, N, FPB, NP, kJitThreads);
-  s += b;
-  s += "  const long long f0 = (long long)blockIdx.x * FPB;\n"
-       "  const int nf = (int)(batch - f0 < FPB ? batch - f0 : FPB);\n"
-       "  cf* A = sm; cf* B = sm + FPB * NP;\n"
-       "  const cf* gi = in + f0 * N; cf* go = out + f0 * N;\n"
-       "  for (int e = threadIdx.x; e < nf * N; e += T) { const cf a = gi[e]; A[(e / N) * NP + e % N] = cf{a.x, csign * a.y}; }\n"
-       "  __syncthreads();\n";
-  emit_stages(s, N, R, S, "nf", NP);
-  s += "  for (int e = threadIdx.x; e < nf * N; e += T) { const cf a = A[(e / N) * NP + e % N]; go[e] = cf{a.x, csign * a.y}; }\n"
-       "}\n";
-  return s;
+namespace {
+// replace every "$NAME" in t by its value
+std::string subst(std::string t, const std::vector<std::pair<std::string, std::string>>& kv) {
+  for (const auto& p : kv) {
+    const std::string key = "$" + p.first;
+    for (size_t at = t.find(key); at != std::string::npos; at = t.find(key, at + p.second.size()))
+      t.replace(at, key.size(), p.second);
+  }
+  return t;
 }
+}  // namespace
 
 // Geometry of a JIT pass kernel: COLS adjacent columns per CTA held in shared memory as
 // [column][row] at an odd pitch LP (conflict-free both along rows and across columns), T threads.
@@ -371,11 +291,11 @@ std::string jit_source(int N) {
 // round), each thread's load/store column stays fixed (T a multiple of COLS), at most 48
 // complex values per thread in registers, <= 100 KB of shared memory (>= 2 CTAs per SM), and
 // the tile large enough to amortise the per-CTA work.
-PassGeo jit_pass_geo(int L, const int* R, int S) {
+PassGeo jit_pass_geo(int L, const int* R, int S, int min_cols) {
   PassGeo best;  // cols == 0: no feasible geometry (callers report UNSUPPORTED_SIZE)
   double bscore = -1.0;
   const int lp = L | 1;
-  for (int cols = 8; cols <= 256; cols *= 2) {
+  for (int cols = min_cols; cols <= 256; cols *= 2) {
     const size_t smem = (size_t)cols * lp * 8;
     if (smem > (size_t)100 * 1024) break;
     for (int T = 64; T <= 512; T += 32) {
@@ -404,8 +324,13 @@ PassGeo jit_pass_geo(int L, const int* R, int S) {
       const int ctas = ctas_reg < ctas_smem ? ctas_reg : ctas_smem;
       if (ctas < 1) continue;
       const double warps = (double)ctas * T / 32.0;
+      // unrolled straight-line work per thread (values through every sub-stage): long kernels
+      // thrash the instruction cache (a 2310-point kernel at ~100 values per thread measured
+      // slower than the looped one it replaced)
+      int work = 0;
+      for (int q = 0; q < S; ++q) work += ((cols * (L / R[q]) + T - 1) / T) * R[q];
       const double score = eff + 0.03 * (tile < 4096 ? tile / 4096 : 1.0) + 0.06 * (warps < 24 ? warps / 24 : 1.0) +
-                           (ctas >= 2 ? 0.1 : 0.0);
+                           (ctas >= 2 ? 0.1 : 0.0) - (work > 64 ? 0.002 * (work - 64) : 0.0);
       if (score > bscore + 1e-9) {
         bscore = score;
         best.cols = cols;
@@ -418,16 +343,129 @@ PassGeo jit_pass_geo(int L, const int* R, int S) {
   return best;
 }
 
+std::string inplace_stages(int L, const int* R, int S, int COLS, int T) {
+  std::string s;
+  int Ns = 1;
+  for (int i = 0; i < S; ++i) {
+    const int Rs = R[i], NB = L / Rs, KB = (COLS * NB + T - 1) / T;
+    const bool exact = (COLS * NB) % T == 0;
+    std::string st = R"(  {  // sub-stage $I: radix $R, Ns $NS, $KB butterfly round(s) per thread
+    cf v[$KB][$R];
+#pragma unroll
+    for (int kb = 0; kb < $KB; ++kb) {
+      const int q = threadIdx.x + kb * T, ff = q / $NB, j = q - ff * $NB;
+      if ($GUARD) {
+#pragma unroll
+        for (int r = 0; r < $R; ++r) v[kb][r] = A[ff * LP + j + r * $NB];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kb = 0; kb < $KB; ++kb) {
+      const int q = threadIdx.x + kb * T, ff = q / $NB, j = q - ff * $NB;
+      if ($GUARD) {
+        const int m = j % $NS;
+$TW        dft$R(v[kb]);
+        const int o = (j / $NS) * $NSR + m;
+#pragma unroll
+        for (int r = 0; r < $R; ++r) A[ff * LP + o + r * $NS] = v[kb][r];
+      }
+    }
+    __syncthreads();
+  }
+)";
+    const std::string tws = Ns > 1 ? "#pragma unroll\n        for (int r = 1; r < " + std::to_string(Rs) +
+                                          "; ++r) v[kb][r] = cmulf(v[kb][r], tw[" + std::to_string(Ns - 1) +
+                                          " + (r - 1) * " + std::to_string(Ns) + " + m]);\n"
+                                    : "";
+    s += subst(st, {{"I", std::to_string(i)},
+                    {"KB", std::to_string(KB)},
+                    {"NSR", std::to_string(Ns * Rs)},
+                    {"NS", std::to_string(Ns)},
+                    {"NB", std::to_string(NB)},
+                    {"GUARD", exact ? "true" : "q < " + std::to_string(COLS * NB)},
+                    {"TW", tws},
+                    {"R", std::to_string(Rs)}});
+    Ns *= Rs;
+  }
+  return s;
+}
+
+// Single-pass kernel generated for N (N <= 4096 with prime factors 11..kJitMaxPrime): FPB whole
+// transforms per CTA (the jit_pass_geo geometry with the transforms as the tile's rows), the
+// contiguous FPB*N tile loaded and stored with coalesced accesses, in-place sub-stages, the
+// inverse's conjugation a separate entry point.
+std::string jit_source(int N) {
+  int R[32];
+  const int S = jit_radices(N, R, 32);
+  if (S < 0) return "";
+  const PassGeo g = jit_pass_geo(N, R, S, 1);
+  if (g.cols <= 0) return "";
+  const int FPB = g.cols, T = g.threads, EL = (FPB * N + T - 1) / T;
+  const int UR = EL < kJitLoadRound ? EL : kJitLoadRound;
+  std::string s = "// generated by libfftc (jit.cpp) for N = " + std::to_string(N) + "\n" + prelude(R, S);
+  s += R"(template <bool C>
+__device__ __forceinline__ void body(const cf* __restrict__ in, cf* __restrict__ out, const cf* __restrict__ tw,
+                                     long long batch) {
+  extern __shared__ cf A[];
+  constexpr int N = $N, LP = $LP, FPB = $FPB, T = $T, EL = $EL, UR = $UR;
+  auto cmulf = [](cf a, cf w) { return cf{fmaf(a.x, w.x, -a.y * w.y), fmaf(a.x, w.y, a.y * w.x)}; };
+  const long long f0 = (long long)blockIdx.x * FPB;
+  const int nf = (int)(batch - f0 < FPB ? batch - f0 : FPB);
+  const int lim = nf * N;  // valid elements of this tile (the last tile may be ragged)
+  const cf* gi = in + f0 * N;
+  cf* go = out + f0 * N;
+#pragma unroll
+  for (int u0 = 0; u0 < EL; u0 += UR) {
+    cf v[UR];
+#pragma unroll
+    for (int k = 0; k < UR; ++k) {
+      const int e = threadIdx.x + (u0 + k) * T;
+      if (u0 + k < EL) v[k] = e < lim ? gi[e] : cf{0.f, 0.f};
+    }
+#pragma unroll
+    for (int k = 0; k < UR; ++k) {
+      const int e = threadIdx.x + (u0 + k) * T;
+      if (u0 + k < EL && ((FPB * N) % T == 0 || e < FPB * N)) {
+        cf x = v[k];
+        if (C) x.y = -x.y;
+        A[(e / N) * LP + e % N] = x;
+      }
+    }
+  }
+  __syncthreads();
+)";
+  s += inplace_stages(N, R, S, FPB, T);
+  s += R"(#pragma unroll
+  for (int u = 0; u < EL; ++u) {
+    const int e = threadIdx.x + u * T;
+    if (e < lim) { const cf a = A[(e / N) * LP + e % N]; go[e] = cf{a.x, C ? -a.y : a.y}; }
+  }
+}
+extern "C" __global__ void __launch_bounds__($T, $MINB) fftc_jit(const cf* __restrict__ in, cf* __restrict__ out,
+    const cf* __restrict__ tw, long long batch, float) { body<false>(in, out, tw, batch); }
+extern "C" __global__ void __launch_bounds__($T, $MINB) fftc_jit_c(const cf* __restrict__ in, cf* __restrict__ out,
+    const cf* __restrict__ tw, long long batch, float) { body<true>(in, out, tw, batch); }
+)";
+  return subst(s, {{"MINB", std::to_string(g.minb)},
+                   {"FPB", std::to_string(FPB)},
+                   {"LP", std::to_string(g.lp)},
+                   {"UR", std::to_string(UR)},
+                   {"EL", std::to_string(EL)},
+                   {"T", std::to_string(T)},
+                   {"N", std::to_string(N)}});
+}
+
 int jit_pass_cols(int L) {
   int R[32];
   const int S = jit_pass_radices(L, R, 32);
-  return S > 0 ? jit_pass_geo(L, R, S).cols : 0;
+  return S > 0 ? jit_pass_geo(L, R, S, 8).cols : 0;
 }
 size_t jit_pass_smem(int L) {
   int R[32];
   const int S = jit_pass_radices(L, R, 32);
   if (S <= 0) return 0;
-  const PassGeo g = jit_pass_geo(L, R, S);
+  const PassGeo g = jit_pass_geo(L, R, S, 8);
   return (size_t)g.cols * g.lp * 8;
 }
 
@@ -440,20 +478,12 @@ size_t jit_pass_smem(int L) {
 // position (c div Ns) Ns L + (c mod Ns) + r Ns.  Each thread loads and stores ONE column f
 // (rows r = rs + u RSTEP), so its twiddles are w^{m rs} times powers of w^{m RSTEP} (a tree:
 // powers 2^b looked up once per thread, every other one a single product).
-namespace {
-// replace every "$NAME" in t by its value
-std::string subst(std::string t, const std::vector<std::pair<std::string, std::string>>& kv) {
-  for (const auto& p : kv) {
-    const std::string key = "$" + p.first;
-    for (size_t at = t.find(key); at != std::string::npos; at = t.find(key, at + p.second.size()))
-      t.replace(at, key.size(), p.second);
-  }
-  return t;
-}
-}  // namespace
 
+// In-place Stockham sub-stages of DFT_L on COLS rows of the tile A[row][element] (pitch LP): KB
+// butterfly rounds per thread, all of a stage's butterflies read into registers before the barrier,
+// then written (one level of Eq. 2, per sub-stage; twiddles from the stage table).
 std::string jit_pass_source(int L, const int* R, int S) {
-  const PassGeo g = jit_pass_geo(L, R, S);
+  const PassGeo g = jit_pass_geo(L, R, S, 8);
   if (g.cols <= 0) return "";
   const int COLS = g.cols, T = g.threads, RSTEP = T / COLS, E = (L + RSTEP - 1) / RSTEP;
   const int UR = E < kJitLoadRound ? E : kJitLoadRound;
@@ -519,50 +549,7 @@ __device__ __forceinline__ void pass_body(const cf* __restrict__ in, cf* __restr
   }
   __syncthreads();
 )";
-  // in-place sub-stages: KB butterfly rounds per thread, all read before the barrier, then written
-  int Ns = 1;
-  for (int i = 0; i < S; ++i) {
-    const int Rs = R[i], NB = L / Rs, KB = (COLS * NB + T - 1) / T;
-    const bool exact = (COLS * NB) % T == 0;
-    std::string st = R"(  {  // sub-stage $I: radix $R, Ns $NS, $KB butterfly round(s) per thread
-    cf v[$KB][$R];
-#pragma unroll
-    for (int kb = 0; kb < $KB; ++kb) {
-      const int q = threadIdx.x + kb * T, ff = q / $NB, j = q - ff * $NB;
-      if ($GUARD) {
-#pragma unroll
-        for (int r = 0; r < $R; ++r) v[kb][r] = A[ff * LP + j + r * $NB];
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int kb = 0; kb < $KB; ++kb) {
-      const int q = threadIdx.x + kb * T, ff = q / $NB, j = q - ff * $NB;
-      if ($GUARD) {
-        const int m = j % $NS;
-$TW        dft$R(v[kb]);
-        const int o = (j / $NS) * $NSR + m;
-#pragma unroll
-        for (int r = 0; r < $R; ++r) A[ff * LP + o + r * $NS] = v[kb][r];
-      }
-    }
-    __syncthreads();
-  }
-)";
-    const std::string tws = Ns > 1 ? "#pragma unroll\n        for (int r = 1; r < " + std::to_string(Rs) +
-                                          "; ++r) v[kb][r] = cmulf(v[kb][r], tw[" + std::to_string(Ns - 1) +
-                                          " + (r - 1) * " + std::to_string(Ns) + " + m]);\n"
-                                    : "";
-    s += subst(st, {{"I", std::to_string(i)},
-                    {"KB", std::to_string(KB)},
-                    {"NSR", std::to_string(Ns * Rs)},
-                    {"NS", std::to_string(Ns)},
-                    {"NB", std::to_string(NB)},
-                    {"GUARD", exact ? "true" : "q < COLS * " + std::to_string(NB)},
-                    {"TW", tws},
-                    {"R", std::to_string(Rs)}});
-    Ns *= Rs;
-  }
+  s += inplace_stages(L, R, S, COLS, T);
   s += R"(  cf* go = out + (long long)bt * N;
   if (FIRST) {  // first pass: column c's L outputs are contiguous at c L + r (lanes walk them)
     cf* gout = go + (long long)c0 * L;
@@ -750,14 +737,22 @@ int jit_compile_src_public(const std::string& src, std::string* cubin, std::stri
 }
 
 const JitKernel* jit_get(int N, cudaError_t* err) {
-  const int fpb = jit_fpb(N);
-  return load_kernel("n:" + std::to_string(N), jit_source(N), "fftc_jit", (size_t)2 * fpb * (N | 1) * 8, N, fpb, err);
+  int R[32];
+  const int S = jit_radices(N, R, 32);
+  const PassGeo g = S > 0 ? jit_pass_geo(N, R, S, 1) : PassGeo{};
+  if (g.cols <= 0) {
+    *err = cudaErrorNotSupported;
+    return nullptr;
+  }
+  static const char* const names[1] = {"fftc_jit_c"};  // variant[0]: the inverse (conjugated)
+  return load_kernel("n:" + std::to_string(N), jit_source(N), "fftc_jit", (size_t)g.cols * g.lp * 8, N, g.cols, err,
+                     names, 1, g.threads);
 }
 
 const JitKernel* jit_pass_get(int L, const int* R, int S, cudaError_t* err) {
   std::string key = "p:" + std::to_string(L);
   for (int i = 0; i < S; ++i) key += ":" + std::to_string(R[i]);
-  const PassGeo g = jit_pass_geo(L, R, S);
+  const PassGeo g = jit_pass_geo(L, R, S, 8);
   if (g.cols <= 0) {
     *err = cudaErrorNotSupported;
     return nullptr;
@@ -804,8 +799,8 @@ cudaError_t jit_launch(const JitKernel* k, const float2* in, float2* out, const 
   if (grid > 0x7fffffffLL) return cudaErrorInvalidValue;
   float csign = conj ? -1.f : 1.f;
   void* args[] = {(void*)&in, (void*)&out, (void*)&tw, (void*)&batch, (void*)&csign};
-  const CUresult r = launch(k->fn, (unsigned)grid, 1, 1, kJitThreads, 1, 1, (unsigned)k->smem, (CUstream)st, args,
-                            nullptr);
+  const CUresult r = launch(conj ? k->variant[0] : k->fn, (unsigned)grid, 1, 1, (unsigned)k->threads, 1, 1,
+                            (unsigned)k->smem, (CUstream)st, args, nullptr);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorLaunchFailure;
 }
 

@@ -28,12 +28,11 @@ struct JitKernel {
 struct PassGeo {
   int cols = 0, threads = 0, lp = 0, minb = 1;
 };
-PassGeo jit_pass_geo(int L, const int* R, int S);
+PassGeo jit_pass_geo(int L, const int* R, int S, int min_cols);  // rows per tile >= min_cols
 
 // Radix schedule for the JIT kernel (16/8/4/2, 9/3, 25/5, 7, then primes 11..kJitMaxPrime),
 // or -1 if N has a prime factor > kJitMaxPrime.
 int jit_radices(int N, int* R, int max);
-int jit_fpb(int N);
 // Radices of a JIT pass kernel of length L: balanced groups of its prime factors.
 int jit_pass_radices(int L, int* R, int max);
 // The straight-line codelet dft<R>(cf* v) the emitter generates (2 <= R <= 128, else "").
