@@ -23,6 +23,8 @@
 //            through shared memory with contiguous 128-bit copies; shared layout
 //            f*(N|1) + i (odd stride -> conflict free across transforms).
 #pragma once
+#include <stdlib.h>
+
 #include <type_traits>
 
 #include "codelets.cuh"
@@ -523,7 +525,12 @@ static cudaError_t launch_fused_batch(const float2* in, float2* out, const float
   auto kern = k_fused_batch<P, DIRECT, MINB>;
   static PerDevice<cudaError_t> attr_pd;
   const cudaError_t attr = attr_pd.get([&] {
-    return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::SMEM);
+    // FFTC_CARVEOUT=<percent> (tuning): the shared-memory share of the unified L1/shared array,
+    // i.e. how much L1 stays for in-flight loads; default: the driver's choice
+    if (const char* c = getenv("FFTC_CARVEOUT"))
+      if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(c));
+    return e;
   });
   if (attr != cudaSuccess) return attr;
   const long long grid = (batch + P::FPB - 1) / P::FPB;
