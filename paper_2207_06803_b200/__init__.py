@@ -314,11 +314,19 @@ class Plan:
                 raise ValueError("%s has %d elements, the plan needs %d" % (name, n, self.elements))
 
     def execute(self, x, out, stream=None):
-        import torch
-        self._check(x, out, cuda=True)
+        """Enqueue the transform of x into out on `stream` (default: torch's current stream of the
+        plan's device).  Both must be contiguous complex64 tensors on the plan's device with at
+        least N*batch elements (checked here: the C ABI receives bare pointers)."""
+        # fast checks first (one call per property; the launch-bound small sizes feel every us)
+        d = self.device
+        if (x.dtype is not _c64() or out.dtype is not _c64() or x.get_device() != d or out.get_device() != d
+                or not x.is_contiguous() or not out.is_contiguous() or x.numel() < self.elements
+                or out.numel() < self.elements):
+            self._check(x, out, cuda=True)  # raises with the precise message
+            raise TypeError("invalid tensors")  # pragma: no cover  (_check always raises here)
         if stream is None:
-            stream = torch.cuda.current_stream(x.device).cuda_stream
-        s = fftc_execute(self.handle, x.data_ptr(), out.data_ptr(), stream)
+            stream = _current_stream(d)
+        s = _lib_fn("fftc_execute")(self.handle, x.data_ptr(), out.data_ptr(), stream)
         if s != FFTC_SUCCESS:
             raise FFTCError(s, "fftc_execute")
         return out
@@ -357,6 +365,34 @@ class Plan:
 
     def __exit__(self, *a):
         self.close()
+
+
+_C64 = None
+_FNS = {}
+
+
+def _c64():
+    global _C64
+    if _C64 is None:
+        import torch
+        _C64 = torch.complex64
+    return _C64
+
+
+def _lib_fn(name):
+    f = _FNS.get(name)
+    if f is None:
+        f = _FNS[name] = getattr(load(), name)
+    return f
+
+
+def _current_stream(device: int) -> int:
+    """Raw cudaStream_t of torch's current stream on `device`."""
+    import torch
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    if raw is not None:
+        return raw(device)
+    return torch.cuda.current_stream(device).cuda_stream
 
 
 def _current_device() -> int:
