@@ -343,10 +343,16 @@ PassGeo jit_pass_geo(int L, const int* R, int S, int min_cols) {
   return best;
 }
 
-std::string inplace_stages(int L, const int* R, int S, int COLS, int T) {
+// In-place Stockham sub-stages s_begin..s_end-1 of DFT_L on COLS rows of the tile A[row][element]
+// (pitch LP): KB butterfly rounds per thread, all of a stage's butterflies read into registers
+// before the barrier, then written (one level of Eq. 2, per sub-stage; twiddles
+// from the stage table).
+std::string inplace_stages(int L, const int* R, int S, int COLS, int T, int s_begin = 0, int s_end = -1) {
   std::string s;
+  if (s_end < 0) s_end = S;
   int Ns = 1;
-  for (int i = 0; i < S; ++i) {
+  for (int i = 0; i < s_begin; ++i) Ns *= R[i];
+  for (int i = s_begin; i < s_end; ++i) {
     const int Rs = R[i], NB = L / Rs, KB = (COLS * NB + T - 1) / T;
     const bool exact = (COLS * NB) % T == 0;
     std::string st = R"(  {  // sub-stage $I: radix $R, Ns $NS, $KB butterfly round(s) per thread
@@ -456,17 +462,158 @@ extern "C" __global__ void __launch_bounds__($T, $MINB) fftc_jit_c(const cf* __r
                    {"N", std::to_string(N)}});
 }
 
-int jit_pass_cols(int L) {
-  int R[32];
-  const int S = jit_pass_radices(L, R, 32);
-  return S > 0 ? jit_pass_geo(L, R, S, 8).cols : 0;
+// Geometry of the fused pass kernel: T = COLS * (L / R_0) threads, so thread (f, j) holds exactly
+// stage 0's butterfly j of column f when it loads rows j + r L/R_0 -- the first sub-stage runs on
+// the loaded registers and the last one stores to HBM from registers (later passes), two
+// shared-memory round trips and a barrier fewer than the generic kernel.  cols == 0: none.
+PassGeo jit_pass_geo_fused(int L, const int* R, int S) {
+  PassGeo best;
+  if (S < 2) return best;
+  const int nb0 = L / R[0], lp = L | 1;
+  double bscore = -1.0;
+  for (int cols = 8; cols <= 128; cols *= 2) {
+    const int T = cols * nb0;
+    const size_t smem = (size_t)cols * lp * 8;
+    if (T > 512 || T < 64 || T % 32 || smem > (size_t)100 * 1024) continue;
+    int vals = R[0];
+    double useful = 0.0, slots = 0.0;
+    bool ok = true;
+    for (int q = 1; q < S; ++q) {
+      const int nb = cols * (L / R[q]), kb = (nb + T - 1) / T;
+      if (kb * R[q] > 32) ok = false;
+      if (kb * R[q] > vals) vals = kb * R[q];
+      useful += (double)nb * R[q];
+      slots += (double)kb * T * R[q];
+    }
+    if (!ok) continue;
+    const int regs = 2 * vals + 48;
+    const int ctas_reg = 65536 / (T * (regs > 64 ? regs : 64));
+    const int ctas_smem = (int)((227 * 1024) / (smem + 1024));
+    const int ctas = ctas_reg < ctas_smem ? ctas_reg : ctas_smem;
+    if (ctas < 1) continue;
+    const double tile = (double)cols * L, warps = (double)ctas * T / 32.0;
+    const double score = useful / slots + 0.03 * (tile < 4096 ? tile / 4096 : 1.0) +
+                         0.06 * (warps < 24 ? warps / 24 : 1.0) + (ctas >= 2 ? 0.1 : 0.0);
+    if (score > bscore + 1e-9) {
+      bscore = score;
+      best.cols = cols;
+      best.threads = T;
+      best.lp = lp;
+      best.minb = ctas >= 2 ? 2 : 1;
+    }
+  }
+  return best;
 }
-size_t jit_pass_smem(int L) {
-  int R[32];
-  const int S = jit_pass_radices(L, R, 32);
-  if (S <= 0) return 0;
-  const PassGeo g = jit_pass_geo(L, R, S, 8);
-  return (size_t)g.cols * g.lp * 8;
+
+// The fused pass kernel (see jit_pass_geo_fused); same entry points and arguments as the
+// generic one below.
+std::string jit_pass_source_fused(int L, const int* R, int S, const PassGeo& g) {
+  const int COLS = g.cols, T = g.threads, R0 = R[0], NB0 = L / R0, RL = R[S - 1], NBL = L / RL;
+  int NsL = 1;
+  for (int i = 0; i < S - 1; ++i) NsL *= R[i];
+  const int KBL = (COLS * NBL + T - 1) / T;
+  std::string s = "// generated by libfftc (jit.cpp): fused pass of length " + std::to_string(L) + "\n" + prelude(R, S);
+  s += R"(template <bool FIRST, bool CI, bool CO>
+__device__ __forceinline__ void pass_body(const cf* __restrict__ in, cf* __restrict__ out, const cf* __restrict__ tw,
+    const cf* __restrict__ twA, const cf* __restrict__ twB, long long N, int Ns, int tws, int tiles, float csign_in,
+    float csign_out) {
+  extern __shared__ cf A[];
+  constexpr int L = $L, LP = $LP, COLS = $COLS, T = $T, R0 = $R0, NB0 = $NB0;
+  const int NB = (int)(N / L);  // columns of this pass (< 2^31)
+  const int bt = (int)(blockIdx.x / tiles);
+  const int c0 = (int)(blockIdx.x - bt * tiles) * COLS;
+  const int nc = NB - c0 < COLS ? NB - c0 : COLS;
+  const int f = threadIdx.x % COLS, j0 = threadIdx.x / COLS;  // column, stage-0 butterfly
+  const int c = c0 + f;
+  const bool fok = f < nc;
+  const long long amask = (1LL << tws) - 1;
+  auto root = [&](long long e) { const cf p = twA[e & amask], q = twB[e >> tws];
+    return cf{fmaf(p.x, q.x, -p.y * q.y), fmaf(p.x, q.y, p.y * q.x)}; };
+  auto cmulf = [](cf a, cf w) { return cf{fmaf(a.x, w.x, -a.y * w.y), fmaf(a.x, w.y, a.y * w.x)}; };
+  {  // sub-stage 0 on the loaded rows j0 + r NB0 of column f
+    cf v[R0];
+    const cf* gp = in + (long long)bt * N + c + (long long)j0 * NB;
+    const long long gstep = (long long)NB0 * NB;
+#pragma unroll
+    for (int r = 0; r < R0; ++r) v[r] = fok ? gp[r * gstep] : cf{0.f, 0.f};
+#pragma unroll
+    for (int r = 0; r < R0; ++r) if (CI) v[r].y = -v[r].y;
+    if (!FIRST) {  // input twiddle w^{m (j0 + r NB0)} = w^{m j0} (w^{m NB0})^r, m = c mod Ns
+      const int cm = c - (c / Ns) * Ns;
+      cf st[R0];
+      st[0] = root((long long)cm * j0);
+      st[1] = root((long long)cm * NB0);
+#pragma unroll
+      for (int r = 2; r < R0; ++r) { int hb = 1; while (2 * hb <= r) hb *= 2;
+        st[r] = r == hb ? cmulf(st[hb / 2], st[hb / 2]) : cmulf(st[hb], st[r - hb]); }
+      v[0] = cmulf(v[0], st[0]);
+#pragma unroll
+      for (int r = 1; r < R0; ++r) v[r] = cmulf(v[r], cmulf(st[0], st[r]));
+    }
+    dft$R0(v);
+#pragma unroll
+    for (int r = 0; r < R0; ++r) A[f * LP + j0 * R0 + r] = v[r];
+  }
+  __syncthreads();
+)";
+  s += inplace_stages(L, R, S, COLS, T, 1, S - 1);
+  s += R"(  cf* go = out + (long long)bt * N;
+  if (FIRST) {  // last sub-stage in place, then column c's contiguous outputs (lanes walk them)
+)";
+  s += inplace_stages(L, R, S, COLS, T, S - 1, S);
+  s += R"(    cf* gout = go + (long long)c0 * L;
+#pragma unroll 4
+    for (int e = threadIdx.x; e < COLS * L; e += T) {
+      const int ff = e / L, r = e - ff * L;
+      if (ff < nc) { const cf a = A[ff * LP + r]; gout[e] = cf{a.x, CO ? -a.y : a.y}; }
+    }
+  } else {  // last sub-stage from shared memory straight to HBM: butterfly (column ff, j), lanes walk ff
+#pragma unroll
+    for (int kb = 0; kb < $KBL; ++kb) {
+      const int q = threadIdx.x + kb * T, ff = q % COLS, j = q / COLS;
+      if ((COLS * $NBL) % T == 0 || q < COLS * $NBL) {
+        cf v[$RL];
+#pragma unroll
+        for (int r = 0; r < $RL; ++r) v[r] = A[ff * LP + j + r * $NBL];
+        const int m = j % $NSL;
+#pragma unroll
+        for (int r = 1; r < $RL; ++r) v[r] = cmulf(v[r], tw[$NSL - 1 + (r - 1) * $NSL + m]);
+        dft$RL(v);
+        if (ff < nc) {  // output row j + r NsL of column cc at (cc div Ns) Ns L + (cc mod Ns) + row Ns
+          const int cc = c0 + ff, cq = cc / Ns, cm = cc - cq * Ns;
+          cf* gs = go + (long long)cq * Ns * L + cm + (long long)j * Ns;
+#pragma unroll
+          for (int r = 0; r < $RL; ++r) gs[(long long)r * $NSL * Ns] = cf{v[r].x, CO ? -v[r].y : v[r].y};
+        }
+      }
+    }
+  }
+}
+)";
+  s += R"(#define FFTC_PASS_ARGS const cf* __restrict__ in, cf* __restrict__ out, const cf* __restrict__ tw, \
+    const cf* __restrict__ twA, const cf* __restrict__ twB, long long N, int Ns, int tws, int tiles, float csign_in, \
+    float csign_out
+#define FFTC_PASS_ENTRY(NAME, FIRST, CI, CO) \
+  extern "C" __global__ void __launch_bounds__($T, $MINB) NAME(FFTC_PASS_ARGS) { \
+    pass_body<FIRST, CI, CO>(in, out, tw, twA, twB, N, Ns, tws, tiles, csign_in, csign_out); }
+FFTC_PASS_ENTRY(fftc_jit_pass, false, false, false)
+FFTC_PASS_ENTRY(fftc_jit_pass_co, false, false, true)
+FFTC_PASS_ENTRY(fftc_jit_pass_first, true, false, false)
+FFTC_PASS_ENTRY(fftc_jit_pass_first_ci, true, true, false)
+FFTC_PASS_ENTRY(fftc_jit_pass_first_cico, true, true, true)
+FFTC_PASS_ENTRY(fftc_jit_pass_first_co, true, false, true)
+)";
+  return subst(s, {{"MINB", std::to_string(g.minb)},
+                   {"COLS", std::to_string(COLS)},
+                   {"KBL", std::to_string(KBL)},
+                   {"NBL", std::to_string(NBL)},
+                   {"NSL", std::to_string(NsL)},
+                   {"NB0", std::to_string(NB0)},
+                   {"LP", std::to_string(g.lp)},
+                   {"RL", std::to_string(RL)},
+                   {"R0", std::to_string(R0)},
+                   {"T", std::to_string(T)},
+                   {"L", std::to_string(L)}});
 }
 
 // One pass of the runtime multi-pass path (the kernel of gpass.cu) with L, its radices and
@@ -478,11 +625,12 @@ size_t jit_pass_smem(int L) {
 // position (c div Ns) Ns L + (c mod Ns) + r Ns.  Each thread loads and stores ONE column f
 // (rows r = rs + u RSTEP), so its twiddles are w^{m rs} times powers of w^{m RSTEP} (a tree:
 // powers 2^b looked up once per thread, every other one a single product).
-
-// In-place Stockham sub-stages of DFT_L on COLS rows of the tile A[row][element] (pitch LP): KB
-// butterfly rounds per thread, all of a stage's butterflies read into registers before the barrier,
-// then written (one level of Eq. 2, per sub-stage; twiddles from the stage table).
+// (the fused variant, jit_pass_source_fused, is used whenever its geometry exists)
 std::string jit_pass_source(int L, const int* R, int S) {
+  if (!getenv("FFTC_JIT_PASS_GENERIC")) {
+    const PassGeo gf = jit_pass_geo_fused(L, R, S);
+    if (gf.cols > 0) return jit_pass_source_fused(L, R, S, gf);
+  }
   const PassGeo g = jit_pass_geo(L, R, S, 8);
   if (g.cols <= 0) return "";
   const int COLS = g.cols, T = g.threads, RSTEP = T / COLS, E = (L + RSTEP - 1) / RSTEP;
@@ -750,9 +898,10 @@ const JitKernel* jit_get(int N, cudaError_t* err) {
 }
 
 const JitKernel* jit_pass_get(int L, const int* R, int S, cudaError_t* err) {
-  std::string key = "p:" + std::to_string(L);
+  std::string key = std::string(getenv("FFTC_JIT_PASS_GENERIC") ? "pg:" : "p:") + std::to_string(L);
   for (int i = 0; i < S; ++i) key += ":" + std::to_string(R[i]);
-  const PassGeo g = jit_pass_geo(L, R, S, 8);
+  PassGeo g = getenv("FFTC_JIT_PASS_GENERIC") ? PassGeo{} : jit_pass_geo_fused(L, R, S);
+  if (g.cols <= 0) g = jit_pass_geo(L, R, S, 8);
   if (g.cols <= 0) {
     *err = cudaErrorNotSupported;
     return nullptr;

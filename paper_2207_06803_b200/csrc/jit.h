@@ -51,8 +51,6 @@ const char* jit_last_log();
 
 // One pass of the runtime multi-pass path (gpass.cu) specialised to its length L and radices
 // (any primes up to kJitMaxPrime), compiled by NVRTC and cached per (L, radices).
-int jit_pass_cols(int L);
-size_t jit_pass_smem(int L);
 constexpr int kJitPassMaxL = 512;  // longest JIT pass (in place, 8 columns); measured: 1000-long passes are slower than three 100-long ones
 std::string jit_pass_source(int L, const int* R, int S);
 const JitKernel* jit_pass_get(int L, const int* R, int S, cudaError_t* err);
