@@ -194,7 +194,7 @@ int fftc_jit_compile(int64_t N, char* log, size_t loglen);
  * length.  Truncation and NUL termination as fftc_jit_source.             */
 int fftc_jit_pass_source(int L, char* buf, size_t len);
 
-/* Host only: compile the JIT pass kernel for pass length L (<= 512, prime factors <= 61;
+/* Host only: compile the JIT pass kernel for pass length L (<= 4096, prime factors <= 61;
  * the runtime multi-pass path above 4096 specialises each pass this way).  Returns the
  * cubin size, or < 0 as fftc_jit_compile.                                 */
 int fftc_jit_pass_compile(int L, char* log, size_t loglen);

@@ -234,7 +234,7 @@ fftc_plan* fftc_plan_create(int64_t N, int64_t batch, int sign) {
   const int Sj = seven_smooth(N) ? -1 : (N <= kGenericMaxN ? jit_radices((int)N, Rj, 32) : -1);
   int Lj[kMaxGPasses];
   const int pj = (!seven_smooth(N) && N > kGenericMaxN)
-                     ? gpass_split(N, Lj, kMaxGPasses, kJitMaxPrime, kJitPassMaxL)
+                     ? gpass_split(N, Lj, kMaxGPasses, kJitMaxPrime, kGpassSplitMaxL)
                      : -1;
   if (!seven_smooth(N) && Sj < 0 && pj < 0) return fail(nullptr, FFTC_ERROR_UNSUPPORTED_SIZE);
   if (batch > 0 && batch > ((int64_t)1 << 60) / (N * 8)) return fail(nullptr, FFTC_ERROR_UNSUPPORTED_SIZE);
@@ -370,8 +370,8 @@ fftc_plan* fftc_plan_create(int64_t N, int64_t batch, int sign) {
     const char* ej = getenv("FFTC_GPASS_JIT");
     const bool jit = jit_available() && !(ej && strcmp(ej, "0") == 0);
     int Lg[kMaxGPasses];
-    // JIT passes run lengths up to kJitPassMaxL = 512 (fewer HBM passes); the compiled kernel 256
-    const int pg = gpass_split(N, Lg, kMaxGPasses, 7, jit ? kJitPassMaxL : kGpassMaxL);
+    // JIT passes run lengths up to kGpassSplitMaxL = 512 (fewer HBM passes); the compiled kernel 256
+    const int pg = gpass_split(N, Lg, kMaxGPasses, 7, jit ? kGpassSplitMaxL : kGpassMaxL);
     if (pg < 0) return fail(p, FFTC_ERROR_UNSUPPORTED_SIZE);
     int R[kMaxGPasses][kMaxStages], S[kMaxGPasses];
     for (int s = 0; s < pg; ++s)  // JIT passes: balanced radices; compiled kernel: the generic set
@@ -627,7 +627,7 @@ int fftc_plan_gpasses(int64_t N, int* lengths, int max) {
   // as the plan does: JIT passes up to 512 long when NVRTC is there, else the compiled 256
   const char* ej = getenv("FFTC_GPASS_JIT");
   const bool jit = jit_available() && !(ej && strcmp(ej, "0") == 0);
-  return gpass_split(N, lengths, max, 7, jit ? kJitPassMaxL : kGpassMaxL);
+  return gpass_split(N, lengths, max, 7, jit ? kGpassSplitMaxL : kGpassMaxL);
 }
 
 int fftc_expr_radices(const char* expr, int64_t* N, int* radices, int max, char* err, size_t errlen) {

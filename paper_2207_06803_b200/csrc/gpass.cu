@@ -13,6 +13,8 @@
 // buffers), and stores with lanes walking columns (Ns > 1: 16 columns are adjacent in the
 // output) or walking r (Ns = 1: a column's outputs are contiguous).  Plain loads/stores,
 // not TMA: for odd N the row pitch N/L * 8 bytes is not a multiple of 16.
+#include <stdlib.h>
+
 #include <vector>
 
 #include "colfft.cuh"
@@ -120,6 +122,19 @@ __global__ void __launch_bounds__(kGpThreads, 4)
 
 int gpass_split(long long N, int* Ls, int max, int max_prime, int max_len) {
   if (N <= 4096) return -1;
+  if (const char* fl = getenv("FFTC_GPASS_LENGTHS")) {  // tuning: explicit pass lengths, e.g. "4096,4096"
+    int q = 0;
+    long long prod = 1;
+    for (const char* c = fl; *c && q < max;) {
+      const int e = atoi(c);
+      if (e < 2 || e > 4096) return -1;
+      Ls[q++] = e;
+      prod *= e;
+      while (*c && *c != ',') ++c;
+      if (*c == ',') ++c;
+    }
+    if (prod == N) return q;
+  }
   std::vector<int> f;
   long long n = N;
   for (int p = max_prime; p >= 2; --p) {

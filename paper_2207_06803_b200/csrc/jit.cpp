@@ -471,7 +471,7 @@ PassGeo jit_pass_geo_fused(int L, const int* R, int S) {
   if (S < 2) return best;
   const int nb0 = L / R[0], lp = L | 1;
   double bscore = -1.0;
-  for (int cols = 8; cols <= 128; cols *= 2) {
+  for (int cols = 2; cols <= 128; cols *= 2) {  // < 8 columns only when nothing wider fits (long passes)
     const int T = cols * nb0;
     const size_t smem = (size_t)cols * lp * 8;
     if (T > 512 || T < 64 || T % 32 || smem > (size_t)100 * 1024) continue;
@@ -493,7 +493,7 @@ PassGeo jit_pass_geo_fused(int L, const int* R, int S) {
     if (ctas < 1) continue;
     const double tile = (double)cols * L, warps = (double)ctas * T / 32.0;
     const double score = useful / slots + 0.03 * (tile < 4096 ? tile / 4096 : 1.0) +
-                         0.06 * (warps < 24 ? warps / 24 : 1.0) + (ctas >= 2 ? 0.1 : 0.0);
+                         0.06 * (warps < 24 ? warps / 24 : 1.0) + (ctas >= 2 ? 0.1 : 0.0) - (cols < 8 ? 0.5 : 0.0);
     if (score > bscore + 1e-9) {
       bscore = score;
       best.cols = cols;

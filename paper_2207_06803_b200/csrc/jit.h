@@ -51,7 +51,8 @@ const char* jit_last_log();
 
 // One pass of the runtime multi-pass path (gpass.cu) specialised to its length L and radices
 // (any primes up to kJitMaxPrime), compiled by NVRTC and cached per (L, radices).
-constexpr int kJitPassMaxL = 512;  // longest JIT pass (in place, 8 columns); measured: 1000-long passes are slower than three 100-long ones
+constexpr int kJitPassMaxL = 4096;  // longest JIT pass kernel (the fused variant, 2 columns, for 4096)
+constexpr int kGpassSplitMaxL = 512;  // longest pass the default split uses (round 1: 1000-long passes were slower than three 100-long ones)
 std::string jit_pass_source(int L, const int* R, int S);
 const JitKernel* jit_pass_get(int L, const int* R, int S, cudaError_t* err);
 cudaError_t jit_pass_launch(const JitKernel* k, const float2* in, float2* out, const float2* tw, const float2* twA,
