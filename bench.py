@@ -431,7 +431,7 @@ def c5_child(args, world):
     if r.returncode != 0 or not lines:
         return {"error": "six-step child job rc=%d: %s" % (r.returncode, (r.stderr or r.stdout)[-400:])}
     d = json.loads(lines[-1])
-    return {k: d[k] for k in ("value", "unit", "ms_per_step", "n_gpus", "variants", "config") if k in d}
+    return {k: d[k] for k in ("value", "unit", "ms_per_step", "n_gpus", "variants", "a2a_reference", "config") if k in d}
 
 
 def run_fftc(args):
@@ -698,10 +698,31 @@ def run_c5_variants(args, D, dev, N):
                     "nvlink_bytes_per_rank_per_a2a": a2a,
                     "nvlink_GBs_per_rank_lower_bound": round(na2a * a2a / t / 1e9, 1), "plan": plan.describe()})
         plan.close()
+    # reference: torch.distributed all_to_all_single (NCCL) of the same 8N/P bytes per rank on the
+    # same ranks -- the measured NVLink rate the six-step's exchanges are compared with
+    ref = None
+    try:
+        src = x.view(torch.float32)
+        dst = torch.empty_like(src)
+        for _ in range(2):
+            D.pg.all_to_all_single(dst, src)
+        torch.cuda.synchronize(dev)
+        D.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(5):
+            D.pg.all_to_all_single(dst, src)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ta = D.max([e0.elapsed_time(e1) / 1e3])[0] / 5
+        ref = {"ms": round(ta * 1e3, 3), "nvlink_GBs_per_rank": round(a2a / ta / 1e9, 1),
+               "note": "torch.distributed.all_to_all_single of 8N/P bytes per rank, (P-1)/P of them over NVLink"}
+    except Exception as e:  # reported, never fatal
+        ref = {"error": "%s: %s" % (type(e).__name__, e)}
     if D.rank == 0:
         best = min(out, key=lambda v: v["ms"])
         print(json.dumps({"metric": METRIC, "value": best["gflops"], "unit": UNIT, "n_gpus": P,
-                          "ms_per_step": best["ms"], "variants": out,
+                          "ms_per_step": best["ms"], "variants": out, "a2a_reference": ref,
                           "config": {"workload": "C5 six-step N=%d over %d ranks" % (N, P)}}), flush=True)
     D.close()
 
