@@ -107,3 +107,63 @@ def test_gpu_gpass_compiled_kernel_without_jit(N, monkeypatch):
         y = y.cpu().numpy()
     err = oracle.rel_l2(y, oracle.fft_ct(x, -1)).max()
     assert err <= min(oracle.tolerance(N), 2e-6), (N, err)
+
+
+
+def _geo(src):
+    import re
+    m = re.search(r"constexpr int L = (\d+), LP = (\d+), COLS = (\d+), T = (\d+)", src)
+    return tuple(int(v) for v in m.groups())
+
+
+@pytest.mark.parametrize("L", [16, 27, 49, 81, 96, 100, 121, 125, 128, 176, 192, 243, 250, 256, 320, 343, 400, 512,
+                               1024, 2048, 4096])
+def test_jit_pass_geometry(L):
+    """The generated pass kernel's tile geometry: an odd pitch >= L, <= 100 KB of shared memory,
+    whole warps; the fused variant's T = COLS * L / R_0 (each thread one stage-0 butterfly)."""
+    src = fftc.fftc_jit_pass_source(L)
+    assert src, L
+    L_, LP, COLS, T = _geo(src)
+    assert L_ == L and LP % 2 == 1 and LP >= L
+    assert COLS * LP * 8 <= 100 * 1024
+    assert T % 32 == 0 and 32 <= T <= 512
+    if "fused pass" in src:
+        import re
+        R0 = int(re.search(r"R0 = (\d+)", src).group(1))
+        assert T == COLS * (L // R0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N,batch", [(6561, 3), (12288, 5), (11 * 4096, 2)])
+def test_gpu_jit_pass_generic_variant(N, batch, monkeypatch):
+    """FFTC_JIT_PASS_GENERIC=1: the non-fused generated pass kernel (staged load / store through
+    shared memory) stays correct, both signs."""
+    torch = pytest.importorskip("torch")
+    monkeypatch.setenv("FFTC_JIT_PASS_GENERIC", "1")
+    x = synth.uniform_c64(N, batch, seed=N % 983)
+    for sign in (-1, 1):
+        with fftc.Plan(N, batch, sign) as p:
+            y = p(torch.from_numpy(x).cuda())
+            torch.cuda.synchronize()
+            y = y.cpu().numpy()
+        err = oracle.rel_l2(y, oracle.fft_ct(x, sign)).max()
+        assert err <= min(oracle.tolerance(N), 2e-6), (N, sign, err)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N,lens", [(1 << 21, "2048,1024"), (1 << 22, "4096,1024"), (3 * (1 << 20), "4096,768")])
+def test_gpu_jit_long_passes(N, lens, monkeypatch):
+    """Generated passes up to 4096 long (FFTC_LARGE=gpass FFTC_GPASS_LENGTHS: the fused kernel on
+    2- and 4-column tiles), both signs, against the oracle."""
+    torch = pytest.importorskip("torch")
+    monkeypatch.setenv("FFTC_LARGE", "gpass")
+    monkeypatch.setenv("FFTC_GPASS_LENGTHS", lens)
+    x = synth.uniform_c64(N, 2, seed=5)
+    for sign in (-1, 1):
+        with fftc.Plan(N, 2, sign) as p:
+            assert "passes=" + lens.split(",")[0] in p.describe(), p.describe()
+            y = p(torch.from_numpy(x).cuda())
+            torch.cuda.synchronize()
+            y = y.cpu().numpy()
+        err = oracle.rel_l2(y, oracle.fft_ct(x, sign)).max()
+        assert err <= min(oracle.tolerance(N), 2e-6), (N, sign, err)
