@@ -103,7 +103,15 @@ constexpr int ilog2(int n) {
 //                  (j = 2p, 2p + 1) and move both with one 128-bit load / store per r
 //   OPT_TW_SHARE : when TPF is a multiple of Ns, a thread's butterflies of a stage share
 //                  m = j mod Ns, so their twiddles are formed once per thread, not per butterfly
-enum SchedOpt : int { OPT_TW_LOAD = 1, OPT_VEC_IO = 2, OPT_TW_SHARE = 4 };
+//   OPT_LD_NA    : direct HBM loads with ld.global.nc.L1::no_allocate (the streamed input does not
+//                  displace the L1-resident twiddle tables)
+enum SchedOpt : int { OPT_TW_LOAD = 1, OPT_VEC_IO = 2, OPT_TW_SHARE = 4, OPT_LD_NA = 8 };
+
+__device__ __forceinline__ float2 ld_na(const float2* p) {
+  float2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+  return v;
+}
 
 template <int N_, class Rad, int TPF_, int FPB_, int MAP_, int PAD_ = 0, int LAY_ = LAY_AUTO, int TAG_ = 0,
           int OPT_ = 0>
@@ -497,7 +505,7 @@ __global__ void __launch_bounds__(P::THREADS, MINB)
     run_stages_io<P>(
         sm, f, lt, fvalid, tw,
         [&](int i, int) {
-          float2 a = __ldcs(gi + i);
+          float2 a = (P::OPT & OPT_LD_NA) ? ld_na(gi + i) : __ldcs(gi + i);
           return make_float2(a.x, csign * a.y);
         },
         [&](int i, float2 v, int) { __stcs(go + i, make_float2(v.x, csign * v.y)); },

@@ -33,6 +33,8 @@ const FusedEntry kTable_mixed[] = {
     FFTC_ENTRY("n210_r15x14_t15x8", 210, Rad_15x14, 15, 8, F_FAST, false, 8, 15, 14),
     FFTC_ENTRY("n210_r15x14_t15x16", 210, Rad_15x14, 15, 16, F_FAST, false, 4, 15, 14),
     // round 2: shared stage twiddles (TPF % Ns == 0), paired 128-bit I/O (even N), all twiddles loaded
+    FFTC_ENTRY_OPT("n2187_r27x9x9_t128x1_na", 2187, Rad_27x9x9, 128, 1, 4, OPT_LD_NA, 27, 9, 9),
+    FFTC_ENTRY_OPT("n3125_r25x5x25_t128x1_na", 3125, Rad_25x5x25, 128, 1, 4, OPT_LD_NA, 25, 5, 25),
     FFTC_ENTRY_OPT("n2187_r27x9x9_t81x2_sh", 2187, Rad_27x9x9, 81, 2, 3, OPT_TW_SHARE, 27, 9, 9),
     FFTC_ENTRY_OPT("n2187_r27x9x9_t81x2_shl", 2187, Rad_27x9x9, 81, 2, 3, OPT_TW_SHARE | OPT_TW_LOAD, 27, 9, 9),
     FFTC_ENTRY_OPT("n2187_r27x9x9_t128x1_l", 2187, Rad_27x9x9, 128, 1, 4, OPT_TW_LOAD, 27, 9, 9),

@@ -16,6 +16,11 @@ namespace fftc {
    Sched<N, RAD, TPF, FPB, MAP, 0, LAY_AUTO, 1>::SMEM,                                                \
    &launch_fused_batch<Sched<N, RAD, TPF, FPB, MAP, 0, LAY_AUTO, 1>, DIRECT, MINB>, NAME}
 
+#define FFTC_ENTRY_PK_OPT(NAME, N, RAD, TPF, FPB, MINB, OPT, ...)                                     \
+  {N, RAD::S, {__VA_ARGS__}, TPF, FPB, TPF * FPB, true,                                               \
+   Sched<N, RAD, TPF, FPB, LT_FAST, 0, LAY_AUTO, 1, OPT>::SMEM,                                        \
+   &launch_fused_batch<Sched<N, RAD, TPF, FPB, LT_FAST, 0, LAY_AUTO, 1, OPT>, true, MINB>, NAME}
+
 extern const FusedEntry kTable_packed[];
 extern const int kCount_packed;
 const FusedEntry kTable_packed[] = {
@@ -24,20 +29,19 @@ const FusedEntry kTable_packed[] = {
     FFTC_ENTRY_PK("n210_r14x15_t15x8d_pk", 210, Rad_14x15, 15, 8, LT_FAST, true, 8, 14, 15),
     FFTC_ENTRY_PK("n1000_r10x10x10_t100x2_pk", 1000, Rad_10x10x10, 100, 2, LT_FAST, true, 4, 10, 10, 10),
     FFTC_ENTRY_PK("n3125_r25x5x25_t128x1_pk", 3125, Rad_25x5x25, 128, 1, LT_FAST, true, 4, 25, 5, 25),
+    // default for 2048: paired FP32 + stage-0 loads with L1::no_allocate (162.9 vs 164.3 us)
+    FFTC_ENTRY_PK_OPT("n2048_r16x16x8_t128x1_pk_na", 2048, Rad_16x16x8, 128, 1, 4, OPT_LD_NA, 16, 16, 8),
     FFTC_ENTRY_PK("n2048_r16x16x8_t128x1_pk", 2048, Rad_16x16x8, 128, 1, LT_FAST, true, 4, 16, 16, 8),
 };
 const int kCount_packed = (int)(sizeof(kTable_packed) / sizeof(kTable_packed[0]));
 
 // paired-FP32 candidates for the other schedules (registered after every scalar table, so
 // they never become defaults; tools/tune.py / FFTC_KERNEL select them)
-#define FFTC_ENTRY_PK_OPT(NAME, N, RAD, TPF, FPB, MINB, OPT, ...)                                     \
-  {N, RAD::S, {__VA_ARGS__}, TPF, FPB, TPF * FPB, true,                                               \
-   Sched<N, RAD, TPF, FPB, LT_FAST, 0, LAY_AUTO, 1, OPT>::SMEM,                                        \
-   &launch_fused_batch<Sched<N, RAD, TPF, FPB, LT_FAST, 0, LAY_AUTO, 1, OPT>, true, MINB>, NAME}
-
 extern const FusedEntry kTable_packed_cand[];
 extern const int kCount_packed_cand;
 const FusedEntry kTable_packed_cand[] = {
+    FFTC_ENTRY_PK_OPT("n3125_r25x5x25_t128x1_pk_na", 3125, Rad_25x5x25, 128, 1, 4, OPT_LD_NA, 25, 5, 25),
+    FFTC_ENTRY_PK_OPT("n1000_r10x10x10_t100x2_pk_na", 1000, Rad_10x10x10, 100, 2, 4, OPT_LD_NA, 10, 10, 10),
     FFTC_ENTRY_PK_OPT("n2187_r27x9x9_t81x2_pk_sh", 2187, Rad_27x9x9, 81, 2, 3, OPT_TW_SHARE, 27, 9, 9),
     FFTC_ENTRY_PK_OPT("n3125_r25x5x25_t125x2_pk_sh", 3125, Rad_25x5x25, 125, 2, 3, OPT_TW_SHARE, 25, 5, 25),
     FFTC_ENTRY_PK_OPT("n1000_r10x10x10_t50x2_pk_vsh", 1000, Rad_10x10x10, 50, 2, 6, OPT_VEC_IO | OPT_TW_SHARE, 10, 10,
