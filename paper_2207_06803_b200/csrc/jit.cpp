@@ -558,14 +558,25 @@ __device__ __forceinline__ void pass_body(const cf* __restrict__ in, cf* __restr
 )";
   s += inplace_stages(L, R, S, COLS, T, 1, S - 1);
   s += R"(  cf* go = out + (long long)bt * N;
-  if (FIRST) {  // last sub-stage in place, then column c's contiguous outputs (lanes walk them)
-)";
-  s += inplace_stages(L, R, S, COLS, T, S - 1, S);
-  s += R"(    cf* gout = go + (long long)c0 * L;
-#pragma unroll 4
-    for (int e = threadIdx.x; e < COLS * L; e += T) {
-      const int ff = e / L, r = e - ff * L;
-      if (ff < nc) { const cf a = A[ff * LP + r]; gout[e] = cf{a.x, CO ? -a.y : a.y}; }
+  if (FIRST) {  // last sub-stage straight to HBM: column c's outputs are contiguous at c L + row, so
+                // butterfly (column ff, j) with lanes walking j stores rows j + r NsL coalesced
+#pragma unroll
+    for (int kb = 0; kb < $KBL; ++kb) {
+      const int q = threadIdx.x + kb * T, ff = q / $NBL, j = q - ff * $NBL;
+      if ((COLS * $NBL) % T == 0 || q < COLS * $NBL) {
+        cf v[$RL];
+#pragma unroll
+        for (int r = 0; r < $RL; ++r) v[r] = A[ff * LP + j + r * $NBL];
+        const int m = j % $NSL;
+#pragma unroll
+        for (int r = 1; r < $RL; ++r) v[r] = cmulf(v[r], tw[$NSL - 1 + (r - 1) * $NSL + m]);
+        dft$RL(v);
+        if (ff < nc) {
+          cf* gs = go + (long long)(c0 + ff) * L + j;
+#pragma unroll
+          for (int r = 0; r < $RL; ++r) gs[r * $NSL] = cf{v[r].x, CO ? -v[r].y : v[r].y};
+        }
+      }
     }
   } else {  // last sub-stage from shared memory straight to HBM: butterfly (column ff, j), lanes walk ff
 #pragma unroll
