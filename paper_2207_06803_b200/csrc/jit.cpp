@@ -401,12 +401,152 @@ $TW        dft$R(v[kb]);
 // transforms per CTA (the jit_pass_geo geometry with the transforms as the tile's rows), the
 // contiguous FPB*N tile loaded and stored with coalesced accesses, in-place sub-stages, the
 // inverse's conjugation a separate entry point.
+// Fused single-pass geometry: T = FPB * (N / R_0) threads, thread (f, j) = stage 0's butterfly j of
+// transform f (lanes along j: its loads a[f N + j + r N/R_0] are coalesced), the last sub-stage
+// stores a[f N + j + r Ns] from registers (also coalesced along j).  cols == 0: none.
+PassGeo jit_single_geo_fused(int N, const int* R, int S) {
+  PassGeo best;
+  // a single-stage N (a prime) has one butterfly per transform: lanes would walk transforms at
+  // stride N, uncoalesced (measured 2x slower for 11, 13, 61) -- the generic kernel stays there
+  if (S < 2) return best;
+  const int nb0 = N / R[0], lp = N | 1;
+  double bscore = -1.0;
+  for (int fpb = 1; fpb <= 256; fpb *= 2) {
+    const int T = fpb * nb0;
+    const size_t smem = S > 1 ? (size_t)fpb * lp * 8 : 0;
+    if (T > 512 || T < 32 || smem > (size_t)100 * 1024) continue;
+    int vals = R[0];
+    double useful = (double)fpb * N, slots = (double)T * R[0];
+    bool ok = true;
+    for (int q = 1; q < S; ++q) {
+      const int nb = fpb * (N / R[q]), kb = (nb + T - 1) / T;
+      if (kb * R[q] > (R[q] > 32 ? R[q] : 32)) ok = false;
+      if (kb * R[q] > vals) vals = kb * R[q];
+      useful += (double)nb * R[q];
+      slots += (double)kb * T * R[q];
+    }
+    if (!ok) continue;
+    const int regs = 2 * vals + 48;
+    const int ctas_reg = 65536 / (T * (regs > 64 ? regs : 64));
+    const int ctas_smem = smem ? (int)((227 * 1024) / (smem + 1024)) : 32;
+    int ctas = ctas_reg < ctas_smem ? ctas_reg : ctas_smem;
+    if (ctas > 32) ctas = 32;
+    if (ctas < 1) continue;
+    const double tile = (double)fpb * N, warps = (double)ctas * ((T + 31) / 32);
+    const double score = useful / slots * ((double)T / (32.0 * ((T + 31) / 32))) +
+                         0.03 * (tile < 4096 ? tile / 4096 : 1.0) + 0.06 * (warps < 24 ? warps / 24 : 1.0) +
+                         (ctas >= 2 ? 0.1 : 0.0);
+    if (score > bscore + 1e-9) {
+      bscore = score;
+      best.cols = fpb;
+      best.threads = T;
+      best.lp = lp;
+      best.minb = ctas >= 2 ? 2 : 1;
+    }
+  }
+  return best;
+}
+
+std::string jit_source_fused(int N, const int* R, int S, const PassGeo& g) {
+  const int FPB = g.cols, T = g.threads, R0 = R[0], NB0 = N / R0, RL = R[S - 1], NBL = N / RL;
+  int NsL = 1;
+  for (int i = 0; i < S - 1; ++i) NsL *= R[i];
+  const int KBL = (FPB * NBL + T - 1) / T;
+  std::string s = "// generated by libfftc (jit.cpp) for N = " + std::to_string(N) + " (fused I/O)\n" + prelude(R, S);
+  s += R"(template <bool C>
+__device__ __forceinline__ void body(const cf* __restrict__ in, cf* __restrict__ out, const cf* __restrict__ tw,
+                                     long long batch) {
+  extern __shared__ cf A[];
+  constexpr int N = $N, LP = $LP, FPB = $FPB, T = $T, R0 = $R0, NB0 = $NB0;
+  auto cmulf = [](cf a, cf w) { return cf{fmaf(a.x, w.x, -a.y * w.y), fmaf(a.x, w.y, a.y * w.x)}; };
+  const long long f0 = (long long)blockIdx.x * FPB;
+  const int nf = (int)(batch - f0 < FPB ? batch - f0 : FPB);
+  const cf* gi = in + f0 * N;
+  cf* go = out + f0 * N;
+  {  // sub-stage 0 on the loaded elements j + r NB0 of transform f
+    const int f = threadIdx.x / NB0, j = threadIdx.x - f * NB0;
+    cf v[R0];
+#pragma unroll
+    for (int r = 0; r < R0; ++r) v[r] = f < nf ? gi[f * N + j + r * NB0] : cf{0.f, 0.f};
+#pragma unroll
+    for (int r = 0; r < R0; ++r) if (C) v[r].y = -v[r].y;
+    dft$R0(v);
+)";
+  if (S == 1) {
+    s += R"(    if (f < nf) {
+#pragma unroll
+      for (int r = 0; r < R0; ++r) go[f * N + j + r * NB0] = cf{v[r].x, C ? -v[r].y : v[r].y};
+    }
+  }
+}
+)";
+  } else {
+    s += R"(#pragma unroll
+    for (int r = 0; r < R0; ++r) A[f * LP + j * R0 + r] = v[r];
+  }
+  __syncthreads();
+)";
+    s += inplace_stages(N, R, S, FPB, T, 1, S - 1);
+    s += R"(#pragma unroll
+  for (int kb = 0; kb < $KBL; ++kb) {  // last sub-stage straight to HBM, lanes along j
+    const int q = threadIdx.x + kb * T, ff = q / $NBL, j = q - ff * $NBL;
+    if ((FPB * $NBL) % T == 0 || q < FPB * $NBL) {
+      cf v[$RL];
+#pragma unroll
+      for (int r = 0; r < $RL; ++r) v[r] = A[ff * LP + j + r * $NBL];
+      const int m = j % $NSL;
+#pragma unroll
+      for (int r = 1; r < $RL; ++r) v[r] = cmulf(v[r], tw[$NSL - 1 + (r - 1) * $NSL + m]);
+      dft$RL(v);
+      if (ff < nf) {
+#pragma unroll
+        for (int r = 0; r < $RL; ++r) go[ff * N + j + r * $NSL] = cf{v[r].x, C ? -v[r].y : v[r].y};
+      }
+    }
+  }
+}
+)";
+  }
+  s += R"(extern "C" __global__ void __launch_bounds__($T, $MINB) fftc_jit(const cf* __restrict__ in, cf* __restrict__ out,
+    const cf* __restrict__ tw, long long batch, float) { body<false>(in, out, tw, batch); }
+extern "C" __global__ void __launch_bounds__($T, $MINB) fftc_jit_c(const cf* __restrict__ in, cf* __restrict__ out,
+    const cf* __restrict__ tw, long long batch, float) { body<true>(in, out, tw, batch); }
+)";
+  return subst(s, {{"MINB", std::to_string(g.minb)},
+                   {"FPB", std::to_string(FPB)},
+                   {"KBL", std::to_string(KBL)},
+                   {"NBL", std::to_string(NBL)},
+                   {"NSL", std::to_string(NsL)},
+                   {"NB0", std::to_string(NB0)},
+                   {"LP", std::to_string(g.lp)},
+                   {"RL", std::to_string(RL)},
+                   {"R0", std::to_string(R0)},
+                   {"T", std::to_string(T)},
+                   {"N", std::to_string(N)}});
+}
+
+// the geometry jit_source and jit_get use: the fused kernel's when one exists (FFTC_JIT_GENERIC=1
+// forces the generic one)
+PassGeo jit_single_geo(int N, const int* R, int S, bool* fused) {
+  *fused = false;
+  if (!getenv("FFTC_JIT_GENERIC")) {
+    const PassGeo gf = jit_single_geo_fused(N, R, S);
+    if (gf.cols > 0) {
+      *fused = true;
+      return gf;
+    }
+  }
+  return jit_pass_geo(N, R, S, 1);
+}
+
 std::string jit_source(int N) {
   int R[32];
   const int S = jit_radices(N, R, 32);
   if (S < 0) return "";
-  const PassGeo g = jit_pass_geo(N, R, S, 1);
+  bool fused = false;
+  const PassGeo g = jit_single_geo(N, R, S, &fused);
   if (g.cols <= 0) return "";
+  if (fused) return jit_source_fused(N, R, S, g);
   const int FPB = g.cols, T = g.threads, EL = (FPB * N + T - 1) / T;
   const int UR = EL < kJitLoadRound ? EL : kJitLoadRound;
   std::string s = "// generated by libfftc (jit.cpp) for N = " + std::to_string(N) + "\n" + prelude(R, S);
@@ -898,14 +1038,16 @@ int jit_compile_src_public(const std::string& src, std::string* cubin, std::stri
 const JitKernel* jit_get(int N, cudaError_t* err) {
   int R[32];
   const int S = jit_radices(N, R, 32);
-  const PassGeo g = S > 0 ? jit_pass_geo(N, R, S, 1) : PassGeo{};
+  bool fused = false;
+  const PassGeo g = S > 0 ? jit_single_geo(N, R, S, &fused) : PassGeo{};
   if (g.cols <= 0) {
     *err = cudaErrorNotSupported;
     return nullptr;
   }
   static const char* const names[1] = {"fftc_jit_c"};  // variant[0]: the inverse (conjugated)
-  return load_kernel("n:" + std::to_string(N), jit_source(N), "fftc_jit", (size_t)g.cols * g.lp * 8, N, g.cols, err,
-                     names, 1, g.threads);
+  const size_t smem = (fused && S == 1) ? 0 : (size_t)g.cols * g.lp * 8;
+  return load_kernel(std::string(fused ? "n:" : "ng:") + std::to_string(N), jit_source(N), "fftc_jit", smem, N,
+                     g.cols, err, names, 1, g.threads);
 }
 
 const JitKernel* jit_pass_get(int L, const int* R, int S, cudaError_t* err) {
