@@ -167,3 +167,21 @@ def test_gpu_jit_long_passes(N, lens, monkeypatch):
             y = y.cpu().numpy()
         err = oracle.rel_l2(y, oracle.fft_ct(x, sign)).max()
         assert err <= min(oracle.tolerance(N), 2e-6), (N, sign, err)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N,batch", [(143, 37), (1088, 5), (3328, 3)])
+def test_gpu_jit_single_pass_generic_variant(N, batch, monkeypatch):
+    """FFTC_JIT_GENERIC=1: the staged single-pass JIT kernel (the fused one is the default for
+    N with two or more stages) stays correct, both signs, ragged last tile."""
+    torch = pytest.importorskip("torch")
+    monkeypatch.setenv("FFTC_JIT_GENERIC", "1")
+    x = synth.uniform_c64(N, batch, seed=N % 977)
+    for sign in (-1, 1):
+        with fftc.Plan(N, batch, sign) as p:
+            assert "kind=jit" in p.describe(), p.describe()
+            y = p(torch.from_numpy(x).cuda())
+            torch.cuda.synchronize()
+            y = y.cpu().numpy()
+        err = oracle.rel_l2(y, oracle.dft_naive(x, sign)).max()
+        assert err <= min(oracle.tolerance(N), 2e-6), (N, sign, err)
