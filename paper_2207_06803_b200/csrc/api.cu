@@ -281,7 +281,21 @@ fftc_plan* fftc_plan_create(int64_t N, int64_t batch, int sign) {
   if (split == 1) {
     int R[kMaxStages];
     const FusedEntry* fe = find_fused((int)N);
-    if (fe) {
+    // 7-smooth N without a compiled schedule: a kernel generated for N (NVRTC; measured 3.3-6.2x
+    // faster than the compiled runtime-schedule kernel, profiles/r02c/smooth_jit.jsonl), unless
+    // NVRTC is missing or FFTC_SMOOTH_JIT=0
+    const char* sj = getenv("FFTC_SMOOTH_JIT");
+    const bool smooth_jit = !fe && jit_available() && !(sj && strcmp(sj, "0") == 0);
+    int Rs[32];
+    const int Ss = smooth_jit ? jit_radices((int)N, Rs, 32) : -1;
+    if (Ss > 0) {
+      p->kind = KIND_JIT;
+      p->jit_S = Ss;
+      for (int s = 0; s < Ss; ++s) p->jit_R[s] = Rs[s];
+      p->jk = jit_get((int)N, &err);
+      if (!p->jk) return fail(p, err == cudaErrorNotSupported ? FFTC_ERROR_UNSUPPORTED_SIZE : from_cuda(err));
+      p->d_tw = upload_stage_table(N, Rs, Ss, &err);
+    } else if (fe) {
       p->kind = KIND_FUSED;
       p->fe = fe;
       p->d_tw = upload_stage_table(N, fe->R, fe->S, &err);

@@ -464,7 +464,7 @@ def test_boundary_errors():
 
 
 def test_describe_and_launches():
-    for N, kind, launches in [(64, "fused", 1), (4096, "fused", 1), (48, "generic", 1), (1 << 20, "passes", 2),
+    for N, kind, launches in [(64, "fused", 1), (4096, "fused", 1), (48, "jit", 1), (1 << 20, "passes", 2),
                               (1 << 24, "passes", 3), (1 << 13, "passes", 2), (1 << 16, "passes", 2),
                               (1 << 22, "passes", 2), (1 << 23, "passes", 2)]:
         with fftc.Plan(N, 2, -1) as p:
@@ -566,3 +566,17 @@ def test_execute_host_many_chunks(monkeypatch):
     assert np.array_equal(out, gpu_fft(x, -1))
     idx = sample_idx(batch)
     check(out[idx], x[idx], -1)
+
+
+@pytest.mark.parametrize("N", [48, 360, 2401, 4000])
+def test_compiled_runtime_schedule_kernel(N, monkeypatch):
+    """FFTC_SMOOTH_JIT=0: 7-smooth N without a compiled schedule on the compiled runtime-schedule
+    kernel (k_generic, the path when NVRTC is missing), ragged batch, both signs."""
+    monkeypatch.setenv("FFTC_SMOOTH_JIT", "0")
+    x = synth.uniform_c64(N, 7, seed=N)
+    for sign in (-1, 1):
+        with fftc.Plan(N, 7, sign) as p:
+            assert "kind=generic" in p.describe(), p.describe()
+            y = p(torch.from_numpy(x).cuda())
+        torch.cuda.synchronize()
+        check(y.cpu().numpy(), x, sign)
