@@ -698,6 +698,20 @@ fftc_plan* fftc_plan_create_radices(int64_t N, int64_t batch, int sign, const in
       p->d_tw = upload_stage_table(N, e->R, e->S, &err);
       return err == cudaSuccess ? p : fail(p, from_cuda(err));
     }
+    // no compiled schedule with exactly these stages: a kernel generated for them (NVRTC), else
+    // the runtime-schedule kernel
+    const char* sj = getenv("FFTC_SMOOTH_JIT");
+    if (jit_available() && !(sj && strcmp(sj, "0") == 0) && S <= 32) {
+      p->jk = jit_get_r((int)N, radices, S, &err);
+      if (p->jk) {
+        p->kind = KIND_JIT;
+        p->jit_S = S;
+        for (int s = 0; s < S; ++s) p->jit_R[s] = radices[s];
+        p->d_tw = upload_stage_table(N, radices, S, &err);
+        return err == cudaSuccess ? p : fail(p, from_cuda(err));
+      }
+      err = cudaSuccess;
+    }
     for (int s = 0; s < S; ++s)
       if (!generic_supports_radix(radices[s])) return fail(p, FFTC_ERROR_UNSUPPORTED_SIZE);
     p->kind = KIND_GENERIC;

@@ -543,6 +543,10 @@ std::string jit_source(int N) {
   int R[32];
   const int S = jit_radices(N, R, 32);
   if (S < 0) return "";
+  return jit_source_r(N, R, S);
+}
+
+std::string jit_source_r(int N, const int* R, int S) {
   bool fused = false;
   const PassGeo g = jit_single_geo(N, R, S, &fused);
   if (g.cols <= 0) return "";
@@ -1038,6 +1042,14 @@ int jit_compile_src_public(const std::string& src, std::string* cubin, std::stri
 const JitKernel* jit_get(int N, cudaError_t* err) {
   int R[32];
   const int S = jit_radices(N, R, 32);
+  if (S <= 0) {
+    *err = cudaErrorNotSupported;
+    return nullptr;
+  }
+  return jit_get_r(N, R, S, err);
+}
+
+const JitKernel* jit_get_r(int N, const int* R, int S, cudaError_t* err) {
   bool fused = false;
   const PassGeo g = S > 0 ? jit_single_geo(N, R, S, &fused) : PassGeo{};
   if (g.cols <= 0) {
@@ -1046,8 +1058,9 @@ const JitKernel* jit_get(int N, cudaError_t* err) {
   }
   static const char* const names[1] = {"fftc_jit_c"};  // variant[0]: the inverse (conjugated)
   const size_t smem = (fused && S == 1) ? 0 : (size_t)g.cols * g.lp * 8;
-  return load_kernel(std::string(fused ? "n:" : "ng:") + std::to_string(N), jit_source(N), "fftc_jit", smem, N,
-                     g.cols, err, names, 1, g.threads);
+  std::string key = std::string(fused ? "n:" : "ng:") + std::to_string(N);
+  for (int i = 0; i < S; ++i) key += ":" + std::to_string(R[i]);
+  return load_kernel(key, jit_source_r(N, R, S), "fftc_jit", smem, N, g.cols, err, names, 1, g.threads);
 }
 
 const JitKernel* jit_pass_get(int L, const int* R, int S, cudaError_t* err) {

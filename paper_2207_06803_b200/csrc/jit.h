@@ -39,12 +39,15 @@ int jit_pass_radices(int L, int* R, int max);
 std::string jit_codelet_source(int R);
 // CUDA C++ source of the kernel specialised to N ("" if unsupported).
 std::string jit_source(int N);
+// ... for an explicit radix list R_0 (leaf) .. R_{S-1} (an FFTc expression's schedule)
+std::string jit_source_r(int N, const int* R, int S);
 // NVRTC compile to an sm_100a cubin (no device needed).  0 on success.
 int jit_compile_cubin(int N, std::string* cubin, std::string* log);
 int jit_compile_src_public(const std::string& src, std::string* cubin, std::string* log);
 bool jit_available();
 // Compiled + loaded kernel for N (cached per process).
 const JitKernel* jit_get(int N, cudaError_t* err);
+const JitKernel* jit_get_r(int N, const int* R, int S, cudaError_t* err);
 cudaError_t jit_launch(const JitKernel* k, const float2* in, float2* out, const float2* tw, long long batch, int conj,
                        cudaStream_t st);
 const char* jit_last_log();
