@@ -280,7 +280,9 @@ fftc_plan* fftc_plan_create(int64_t N, int64_t batch, int sign) {
   const int split = top_split(N, &M, &K);
   if (split == 1) {
     int R[kMaxStages];
-    const FusedEntry* fe = find_fused((int)N);
+    // FFTC_FORCE_JIT=1 (tuning): the generated kernel even where a compiled schedule exists
+    const char* fj = getenv("FFTC_FORCE_JIT");
+    const FusedEntry* fe = (fj && strcmp(fj, "1") == 0) ? nullptr : find_fused((int)N);
     // 7-smooth N without a compiled schedule: a kernel generated for N (NVRTC; measured 3.3-6.2x
     // faster than the compiled runtime-schedule kernel, profiles/r02c/smooth_jit.jsonl), unless
     // NVRTC is missing or FFTC_SMOOTH_JIT=0

@@ -291,10 +291,30 @@ std::string subst(std::string t, const std::vector<std::pair<std::string, std::s
 // round), each thread's load/store column stays fixed (T a multiple of COLS), at most 48
 // complex values per thread in registers, <= 100 KB of shared memory (>= 2 CTAs per SM), and
 // the tile large enough to amortise the per-CTA work.
-PassGeo jit_pass_geo(int L, const int* R, int S, int min_cols) {
+// Shared-memory layout of the generated kernels: row f, element i at f LP + i + i / P (macro SIDX).
+// Single-pass kernels walk a transform's butterflies with consecutive lanes, so sub-stage 0 writes
+// i = j R_0 + r at a lane stride of R_0 elements: when 4 | R_0 that is a 4- to 16-way bank
+// conflict, and one pad element every P = R_0 (power of two) or 16 elements removes it.  Pass
+// kernels load and store across columns (no such stride) and odd R_0 is conflict free: no padding
+// (P = 0).  The row pitch LP >= L + L / P is odd (conflict free across rows).
+int jit_padp(const int* R, bool single) {
+  if (!single || R[0] % 4 != 0) return 0;
+  return (R[0] & (R[0] - 1)) == 0 ? R[0] : 16;
+}
+int jit_pitch(int L, const int* R, bool single) {
+  const int p = jit_padp(R, single);
+  return (L + (p ? L / p : 0)) | 1;
+}
+std::string jit_sidx_macro(const int* R, bool single) {
+  const int p = jit_padp(R, single);
+  return p ? "#define SIDX(f, i) ((f) * LP + (i) + (i) / " + std::to_string(p) + ")\n"
+           : std::string("#define SIDX(f, i) ((f) * LP + (i))\n");
+}
+
+PassGeo jit_pass_geo(int L, const int* R, int S, int min_cols, bool single) {
   PassGeo best;  // cols == 0: no feasible geometry (callers report UNSUPPORTED_SIZE)
   double bscore = -1.0;
-  const int lp = L | 1;
+  const int lp = jit_pitch(L, R, single);
   for (int cols = min_cols; cols <= 256; cols *= 2) {
     const size_t smem = (size_t)cols * lp * 8;
     if (smem > (size_t)100 * 1024) break;
@@ -362,7 +382,7 @@ std::string inplace_stages(int L, const int* R, int S, int COLS, int T, int s_be
       const int q = threadIdx.x + kb * T, ff = q / $NB, j = q - ff * $NB;
       if ($GUARD) {
 #pragma unroll
-        for (int r = 0; r < $R; ++r) v[kb][r] = A[ff * LP + j + r * $NB];
+        for (int r = 0; r < $R; ++r) v[kb][r] = A[SIDX(ff, j + r * $NB)];
       }
     }
     __syncthreads();
@@ -374,7 +394,7 @@ std::string inplace_stages(int L, const int* R, int S, int COLS, int T, int s_be
 $TW        dft$R(v[kb]);
         const int o = (j / $NS) * $NSR + m;
 #pragma unroll
-        for (int r = 0; r < $R; ++r) A[ff * LP + o + r * $NS] = v[kb][r];
+        for (int r = 0; r < $R; ++r) A[SIDX(ff, o + r * $NS)] = v[kb][r];
       }
     }
     __syncthreads();
@@ -409,7 +429,7 @@ PassGeo jit_single_geo_fused(int N, const int* R, int S) {
   // a single-stage N (a prime) has one butterfly per transform: lanes would walk transforms at
   // stride N, uncoalesced (measured 2x slower for 11, 13, 61) -- the generic kernel stays there
   if (S < 2) return best;
-  const int nb0 = N / R[0], lp = N | 1;
+  const int nb0 = N / R[0], lp = jit_pitch(N, R, true);
   double bscore = -1.0;
   for (int fpb = 1; fpb <= 256; fpb *= 2) {
     const int T = fpb * nb0;
@@ -452,7 +472,7 @@ std::string jit_source_fused(int N, const int* R, int S, const PassGeo& g) {
   int NsL = 1;
   for (int i = 0; i < S - 1; ++i) NsL *= R[i];
   const int KBL = (FPB * NBL + T - 1) / T;
-  std::string s = "// generated by libfftc (jit.cpp) for N = " + std::to_string(N) + " (fused I/O)\n" + prelude(R, S);
+  std::string s = "// generated by libfftc (jit.cpp) for N = " + std::to_string(N) + " (fused I/O)\n" + prelude(R, S) + jit_sidx_macro(R, true);
   s += R"(template <bool C>
 __device__ __forceinline__ void body(const cf* __restrict__ in, cf* __restrict__ out, const cf* __restrict__ tw,
                                      long long batch) {
@@ -482,7 +502,7 @@ __device__ __forceinline__ void body(const cf* __restrict__ in, cf* __restrict__
 )";
   } else {
     s += R"(#pragma unroll
-    for (int r = 0; r < R0; ++r) A[f * LP + j * R0 + r] = v[r];
+    for (int r = 0; r < R0; ++r) A[SIDX(f, j * R0 + r)] = v[r];
   }
   __syncthreads();
 )";
@@ -493,7 +513,7 @@ __device__ __forceinline__ void body(const cf* __restrict__ in, cf* __restrict__
     if ((FPB * $NBL) % T == 0 || q < FPB * $NBL) {
       cf v[$RL];
 #pragma unroll
-      for (int r = 0; r < $RL; ++r) v[r] = A[ff * LP + j + r * $NBL];
+      for (int r = 0; r < $RL; ++r) v[r] = A[SIDX(ff, j + r * $NBL)];
       const int m = j % $NSL;
 #pragma unroll
       for (int r = 1; r < $RL; ++r) v[r] = cmulf(v[r], tw[$NSL - 1 + (r - 1) * $NSL + m]);
@@ -536,7 +556,7 @@ PassGeo jit_single_geo(int N, const int* R, int S, bool* fused) {
       return gf;
     }
   }
-  return jit_pass_geo(N, R, S, 1);
+  return jit_pass_geo(N, R, S, 1, true);
 }
 
 std::string jit_source(int N) {
@@ -553,7 +573,7 @@ std::string jit_source_r(int N, const int* R, int S) {
   if (fused) return jit_source_fused(N, R, S, g);
   const int FPB = g.cols, T = g.threads, EL = (FPB * N + T - 1) / T;
   const int UR = EL < kJitLoadRound ? EL : kJitLoadRound;
-  std::string s = "// generated by libfftc (jit.cpp) for N = " + std::to_string(N) + "\n" + prelude(R, S);
+  std::string s = "// generated by libfftc (jit.cpp) for N = " + std::to_string(N) + "\n" + prelude(R, S) + jit_sidx_macro(R, true);
   s += R"(template <bool C>
 __device__ __forceinline__ void body(const cf* __restrict__ in, cf* __restrict__ out, const cf* __restrict__ tw,
                                      long long batch) {
@@ -579,7 +599,7 @@ __device__ __forceinline__ void body(const cf* __restrict__ in, cf* __restrict__
       if (u0 + k < EL && ((FPB * N) % T == 0 || e < FPB * N)) {
         cf x = v[k];
         if (C) x.y = -x.y;
-        A[(e / N) * LP + e % N] = x;
+        A[SIDX(e / N, e % N)] = x;
       }
     }
   }
@@ -589,7 +609,7 @@ __device__ __forceinline__ void body(const cf* __restrict__ in, cf* __restrict__
   s += R"(#pragma unroll
   for (int u = 0; u < EL; ++u) {
     const int e = threadIdx.x + u * T;
-    if (e < lim) { const cf a = A[(e / N) * LP + e % N]; go[e] = cf{a.x, C ? -a.y : a.y}; }
+    if (e < lim) { const cf a = A[SIDX(e / N, e % N)]; go[e] = cf{a.x, C ? -a.y : a.y}; }
   }
 }
 extern "C" __global__ void __launch_bounds__($T, $MINB) fftc_jit(const cf* __restrict__ in, cf* __restrict__ out,
@@ -613,7 +633,7 @@ extern "C" __global__ void __launch_bounds__($T, $MINB) fftc_jit_c(const cf* __r
 PassGeo jit_pass_geo_fused(int L, const int* R, int S) {
   PassGeo best;
   if (S < 2) return best;
-  const int nb0 = L / R[0], lp = L | 1;
+  const int nb0 = L / R[0], lp = jit_pitch(L, R, false);
   double bscore = -1.0;
   for (int cols = 2; cols <= 128; cols *= 2) {  // < 8 columns only when nothing wider fits (long passes)
     const int T = cols * nb0;
@@ -656,7 +676,7 @@ std::string jit_pass_source_fused(int L, const int* R, int S, const PassGeo& g) 
   int NsL = 1;
   for (int i = 0; i < S - 1; ++i) NsL *= R[i];
   const int KBL = (COLS * NBL + T - 1) / T;
-  std::string s = "// generated by libfftc (jit.cpp): fused pass of length " + std::to_string(L) + "\n" + prelude(R, S);
+  std::string s = "// generated by libfftc (jit.cpp): fused pass of length " + std::to_string(L) + "\n" + prelude(R, S) + jit_sidx_macro(R, false);
   s += R"(template <bool FIRST, bool CI, bool CO>
 __device__ __forceinline__ void pass_body(const cf* __restrict__ in, cf* __restrict__ out, const cf* __restrict__ tw,
     const cf* __restrict__ twA, const cf* __restrict__ twB, long long N, int Ns, int tws, int tiles, float csign_in,
@@ -696,7 +716,7 @@ __device__ __forceinline__ void pass_body(const cf* __restrict__ in, cf* __restr
     }
     dft$R0(v);
 #pragma unroll
-    for (int r = 0; r < R0; ++r) A[f * LP + j0 * R0 + r] = v[r];
+    for (int r = 0; r < R0; ++r) A[SIDX(f, j0 * R0 + r)] = v[r];
   }
   __syncthreads();
 )";
@@ -710,7 +730,7 @@ __device__ __forceinline__ void pass_body(const cf* __restrict__ in, cf* __restr
       if ((COLS * $NBL) % T == 0 || q < COLS * $NBL) {
         cf v[$RL];
 #pragma unroll
-        for (int r = 0; r < $RL; ++r) v[r] = A[ff * LP + j + r * $NBL];
+        for (int r = 0; r < $RL; ++r) v[r] = A[SIDX(ff, j + r * $NBL)];
         const int m = j % $NSL;
 #pragma unroll
         for (int r = 1; r < $RL; ++r) v[r] = cmulf(v[r], tw[$NSL - 1 + (r - 1) * $NSL + m]);
@@ -729,7 +749,7 @@ __device__ __forceinline__ void pass_body(const cf* __restrict__ in, cf* __restr
       if ((COLS * $NBL) % T == 0 || q < COLS * $NBL) {
         cf v[$RL];
 #pragma unroll
-        for (int r = 0; r < $RL; ++r) v[r] = A[ff * LP + j + r * $NBL];
+        for (int r = 0; r < $RL; ++r) v[r] = A[SIDX(ff, j + r * $NBL)];
         const int m = j % $NSL;
 #pragma unroll
         for (int r = 1; r < $RL; ++r) v[r] = cmulf(v[r], tw[$NSL - 1 + (r - 1) * $NSL + m]);
@@ -786,11 +806,11 @@ std::string jit_pass_source(int L, const int* R, int S) {
     const PassGeo gf = jit_pass_geo_fused(L, R, S);
     if (gf.cols > 0) return jit_pass_source_fused(L, R, S, gf);
   }
-  const PassGeo g = jit_pass_geo(L, R, S, 8);
+  const PassGeo g = jit_pass_geo(L, R, S, 8, false);
   if (g.cols <= 0) return "";
   const int COLS = g.cols, T = g.threads, RSTEP = T / COLS, E = (L + RSTEP - 1) / RSTEP;
   const int UR = E < kJitLoadRound ? E : kJitLoadRound;
-  std::string s = "// generated by libfftc (jit.cpp): pass of length " + std::to_string(L) + "\n" + prelude(R, S);
+  std::string s = "// generated by libfftc (jit.cpp): pass of length " + std::to_string(L) + "\n" + prelude(R, S) + jit_sidx_macro(R, false);
   // the body is a template on FIRST (pass 0: Ns = 1, no input twiddle, contiguous column
   // outputs); fftc_jit_pass_first / fftc_jit_pass instantiate it, so neither carries the other's
   // code under a runtime predicate
@@ -845,7 +865,7 @@ __device__ __forceinline__ void pass_body(const cf* __restrict__ in, cf* __restr
             if ((u & 7) == 0 || k == 0) base = root((long long)cm * (rs + (u & ~7) * RSTEP));
             x = (u & 7) ? cmulf(x, cmulf(base, st[u & 7])) : cmulf(x, base);
           }
-          A[f * LP + r] = x;  // columns >= nc carry zeros: computed, never stored to HBM
+          A[SIDX(f, r)] = x;  // columns >= nc carry zeros: computed, never stored to HBM
         }
       }
     }
@@ -859,7 +879,7 @@ __device__ __forceinline__ void pass_body(const cf* __restrict__ in, cf* __restr
 #pragma unroll 4
     for (int e = threadIdx.x; e < COLS * L; e += T) {
       const int ff = e / L, r = e - ff * L;
-      if (ff < nc) { const cf a = A[ff * LP + r]; gout[e] = cf{a.x, CO ? -a.y : a.y}; }
+      if (ff < nc) { const cf a = A[SIDX(ff, r)]; gout[e] = cf{a.x, CO ? -a.y : a.y}; }
     }
   } else if (fok) {  // autosort position (c div Ns) Ns L + (c mod Ns) + r Ns (lanes walk c)
     cf* gs = go + (long long)cq * Ns * L + cm + (long long)rs * Ns;
@@ -867,7 +887,7 @@ __device__ __forceinline__ void pass_body(const cf* __restrict__ in, cf* __restr
 #pragma unroll
     for (int u = 0; u < E; ++u) {
       const int r = rs + u * RSTEP;
-      if (L % RSTEP == 0 || r < L) { const cf a = A[f * LP + r]; gs[u * sstep] = cf{a.x, CO ? -a.y : a.y}; }
+      if (L % RSTEP == 0 || r < L) { const cf a = A[SIDX(f, r)]; gs[u * sstep] = cf{a.x, CO ? -a.y : a.y}; }
     }
   }
 }
@@ -1067,7 +1087,7 @@ const JitKernel* jit_pass_get(int L, const int* R, int S, cudaError_t* err) {
   std::string key = std::string(getenv("FFTC_JIT_PASS_GENERIC") ? "pg:" : "p:") + std::to_string(L);
   for (int i = 0; i < S; ++i) key += ":" + std::to_string(R[i]);
   PassGeo g = getenv("FFTC_JIT_PASS_GENERIC") ? PassGeo{} : jit_pass_geo_fused(L, R, S);
-  if (g.cols <= 0) g = jit_pass_geo(L, R, S, 8);
+  if (g.cols <= 0) g = jit_pass_geo(L, R, S, 8, false);
   if (g.cols <= 0) {
     *err = cudaErrorNotSupported;
     return nullptr;

@@ -28,7 +28,7 @@ struct JitKernel {
 struct PassGeo {
   int cols = 0, threads = 0, lp = 0, minb = 1;
 };
-PassGeo jit_pass_geo(int L, const int* R, int S, int min_cols);  // rows per tile >= min_cols
+PassGeo jit_pass_geo(int L, const int* R, int S, int min_cols, bool single);  // rows per tile >= min_cols
 
 // Radix schedule for the JIT kernel (16/8/4/2, 9/3, 25/5, 7, then primes 11..kJitMaxPrime),
 // or -1 if N has a prime factor > kJitMaxPrime.
