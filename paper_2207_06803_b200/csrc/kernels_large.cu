@@ -14,7 +14,10 @@ const FusedEntry kTable_large[] = {
     FFTC_ENTRY("n2048_r16x16x8_t128x2", 2048, Rad_16x16x8, 128, 2, LT_FAST, true, 3, 16, 16, 8),
     FFTC_TMA("n2048_r8x16x16_t128x1_tma", 2048, Rad_8x16x16, 128, 1, 6, 8, 16, 16),
     FFTC_PIPE("n2048_r16x16x8_t128x1_pipe3", 2048, Rad_16x16x8, 128, 1, 3, 16, 16, 8),
-    // default: stage-0 loads with L1::no_allocate (measured 180.7 vs 182.7 us, profiles/r02b/ld_na.jsonl)
+    // default: 256 threads, stage-0 loads with L1::no_allocate (interleaved A/B on one box: 179.8 vs
+    // 182.6 us for the 128-thread no_allocate kernel and 180.4 for 256 threads with plain loads,
+    // profiles/r02b/defaults_ab.jsonl)
+    FFTC_ENTRY_OPT("n4096_r16x16x16_t256x1_na", 4096, Rad_16x16x16, 256, 1, 3, OPT_LD_NA, 16, 16, 16),
     FFTC_ENTRY_OPT("n4096_r16x16x16_t128x1_na", 4096, Rad_16x16x16, 128, 1, 4, OPT_LD_NA, 16, 16, 16),
     FFTC_ENTRY("n4096_r16x16x16_t128x1", 4096, Rad_16x16x16, 128, 1, LT_FAST, true, 4, 16, 16, 16),
     FFTC_ENTRY("n4096_r16x16x16_t256x1", 4096, Rad_16x16x16, 256, 1, LT_FAST, true, 3, 16, 16, 16),

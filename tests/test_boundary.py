@@ -167,7 +167,8 @@ def test_default_schedules_follow_the_measured_policy():
     they measured faster on B200, the scalar schedules elsewhere; the warp-shuffle
     exchange for N = 64 and L1::no_allocate stage-0 loads for 2048 / 4096 (DESIGN §6 K1)."""
     packed = {128, 105, 210, 1000, 3125, 2048}
-    special = {64: "n64_r8x8_t8x8_shfl", 2048: "n2048_r16x16x8_t128x1_pk_na", 4096: "n4096_r16x16x16_t128x1_na"}
+    special = {64: "n64_r8x8_t8x8_shfl", 2048: "n2048_r16x16x8_t128x1_pk_na", 4096: "n4096_r16x16x16_t256x1_na",
+               60: "n60_r4x15_t4x16"}
     for N in (8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096, 60, 105, 210, 1000, 2187, 3125):
         names = fftc.fftc_candidates(N)
         assert names, N
