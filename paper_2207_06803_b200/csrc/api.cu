@@ -290,12 +290,13 @@ fftc_plan* fftc_plan_create(int64_t N, int64_t batch, int sign) {
     const bool smooth_jit = !fe && jit_available() && !(sj && strcmp(sj, "0") == 0);
     int Rs[32];
     const int Ss = smooth_jit ? jit_radices((int)N, Rs, 32) : -1;
-    if (Ss > 0) {
+    const JitKernel* jk = Ss > 0 ? jit_get((int)N, &err) : nullptr;
+    err = cudaSuccess;  // a generated kernel that cannot be built falls back to the compiled one
+    if (jk) {
       p->kind = KIND_JIT;
       p->jit_S = Ss;
       for (int s = 0; s < Ss; ++s) p->jit_R[s] = Rs[s];
-      p->jk = jit_get((int)N, &err);
-      if (!p->jk) return fail(p, err == cudaErrorNotSupported ? FFTC_ERROR_UNSUPPORTED_SIZE : from_cuda(err));
+      p->jk = jk;
       p->d_tw = upload_stage_table(N, Rs, Ss, &err);
     } else if (fe) {
       p->kind = KIND_FUSED;
