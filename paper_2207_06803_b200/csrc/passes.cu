@@ -201,6 +201,8 @@ static const PassEntry kPasses[] = {
     FFTC_PASS2("p4096_r16x16x16_c2b2", 4096, PRad_16x16x16, 256, 1, 2, 16, 16, 16),
     FFTC_PASS4("p2048_r16x16x8_c4b3", 2048, PRad_16x16x8, 128, 1, 3, 16, 16, 8),
     FFTC_PASS4("p4096_r16x16x16_c4b1", 4096, PRad_16x16x16, 128, 1, 1, 16, 16, 16),
+    // a cluster of 4 CTAs per 8-column tile, each the 1024-point sub-DFT of one row residue class
+    {4096, 2, {32, 32}, 32, 8, &launch_cpass4096, "cp4096_q4_r32x32_c8b2", 4},
 };
 
 // the entry of length L among a comma-separated list of candidate names
@@ -275,6 +277,20 @@ static bool map_in(CUtensorMap* m, const void* base, long long N, int L, int C, 
   cuuint32_t box[3] = {(cuuint32_t)C, (cuuint32_t)(L < 256 ? L : 256), 1};
   cuuint32_t es[3] = {1, 1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_INT64, 3, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, tile_swizzle(C), CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// cluster pass input: rows r = Q i + q of the [batch][L rows][NB cols] view as a (c, q, i, batch)
+// view, box [C cols][1][256 rows][1] -- CTA q of a cluster loads only its residue class
+static bool map_in_cluster(CUtensorMap* m, const void* base, long long N, int L, int C, int Q, long long batch) {
+  encode_fn enc = get_encode();
+  if (!enc) return false;
+  const long long NB = N / L;
+  cuuint64_t dims[4] = {(cuuint64_t)NB, (cuuint64_t)Q, (cuuint64_t)(L / Q), (cuuint64_t)batch};
+  cuuint64_t strides[3] = {(cuuint64_t)NB * 8, (cuuint64_t)Q * NB * 8, (cuuint64_t)N * 8};
+  cuuint32_t box[4] = {(cuuint32_t)C, 1, 256, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_INT64, 4, const_cast<void*>(base), dims, strides, box, es,
              CU_TENSOR_MAP_INTERLEAVE_NONE, tile_swizzle(C), CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -386,9 +402,14 @@ cudaError_t passes_execute(const PassPlanData& pp, const float2* in, float2* out
     const PassEntry* e = pp.e[s];
     const int L = e->L;
     CUtensorMap tin, tout;
-    if (!map_in(&tin, src, pp.N, L, e->cols, batch)) return cudaErrorInvalidValue;
-    if (s > 0 && !map_out(&tout, dst, pp.N, L, e->cols, Ns, batch)) return cudaErrorInvalidValue;
-    if (s == 0 && !map_out0(&tout, dst, pp.N, L, e->cols, batch)) return cudaErrorInvalidValue;
+    if (e->cluster) {  // loads of one row residue class per CTA; outputs stored by the threads
+      if (!map_in_cluster(&tin, src, pp.N, L, e->cols, e->cluster, batch)) return cudaErrorInvalidValue;
+      tout = tin;
+    } else {
+      if (!map_in(&tin, src, pp.N, L, e->cols, batch)) return cudaErrorInvalidValue;
+      if (s > 0 && !map_out(&tout, dst, pp.N, L, e->cols, Ns, batch)) return cudaErrorInvalidValue;
+      if (s == 0 && !map_out0(&tout, dst, pp.N, L, e->cols, batch)) return cudaErrorInvalidValue;
+    }
     PassGeom g{};
     g.tiles_per_batch = (int)(pp.N / L / e->cols);
     g.tiles_total = batch * g.tiles_per_batch;

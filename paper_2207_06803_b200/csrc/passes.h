@@ -28,7 +28,14 @@ struct PassEntry {
   int cols;  // columns per tile (16: 128-byte rows; 8: 64-byte rows)
   pass_launch_fn launch;
   const char* name;
+  int cluster = 0;  // > 0: a cluster of this many CTAs shares each tile's columns (cpass.cu)
 };
+
+// 4096-long pass on a cluster of four CTAs (cpass.cu): each CTA loads the rows = q (mod 4) of
+// 8 columns through a 4-D tensor map (tin), writes its outputs straight to `out`
+cudaError_t launch_cpass4096(bool first, const CUtensorMap& tin, const CUtensorMap& tout, float2* out,
+                             const float2* tw, const float2* twA, const float2* twB, const PassGeom& g, int conj_in,
+                             int conj_out, cudaStream_t st);
 
 constexpr int kMaxPasses = 6;
 struct PassPlanData {

@@ -55,11 +55,14 @@ __device__ __forceinline__ PassTwPre pass_tw_pre(int c, int lt, int Ns, const fl
   return t;
 }
 
+// rmul / roff: the tile's row i is row rmul i + roff of the pass's column (a CTA of a cluster
+// holding one residue class of the rows, cpass.cu); the input twiddle is w^{m (rmul i + roff)}.
 template <class P, bool TW, bool OUT0 = false>
 __device__ __forceinline__ void pass_tile(float2* sm, int f, int lt, int c, int Ns,
                                           const float2* __restrict__ tw, const float2* __restrict__ twA,
                                           const float2* __restrict__ twB, int tws, float csign_in,
-                                          float csign_out, const PassTwPre* pre = nullptr) {
+                                          float csign_out, const PassTwPre* pre = nullptr, int rmul = 1,
+                                          int roff = 0) {
   static_assert((P::FPB == 16 && P::LAY == LAY_TMA128) || (P::FPB == 8 && P::LAY == LAY_TMA64) ||
                     ((P::FPB == 2 || P::FPB == 4) && P::LAY == LAY_TMA16 && P::S >= 2),
                 "pass tiles: 16 columns with the TMA 128B swizzle, 8 with the 64B swizzle, or 2/4 (linear)");
@@ -77,7 +80,7 @@ __device__ __forceinline__ void pass_tile(float2* sm, int f, int lt, int c, int 
         sp[bb] = pre->sp[bb];
       });
     } else {
-      sp[0] = root_lookup_s(twA, twB, m * NB0, tws);
+      sp[0] = root_lookup_s(twA, twB, m * rmul * NB0, tws);
       sfor<NB2 - 1>([&](auto b_) {
         constexpr int bb = decltype(b_)::value + 1;
         sp[bb] = cmul(sp[bb - 1], sp[bb - 1]);
@@ -93,7 +96,7 @@ __device__ __forceinline__ void pass_tile(float2* sm, int f, int lt, int c, int 
     v.y *= csign_in;
     if constexpr (TW) {
       if (r == 0) {
-        wt[0] = pre ? pre->base : root_lookup_s(twA, twB, m * i, tws);
+        wt[0] = pre ? pre->base : root_lookup_s(twA, twB, m * ((long long)rmul * i + roff), tws);
       } else {
         int hb = 1, b = 0;
         while (2 * hb <= r) {

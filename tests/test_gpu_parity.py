@@ -153,6 +153,23 @@ def test_long_pass_narrow_tiles(logs, later, monkeypatch):
         check(gpu_fft(x, sign)[idx], x[idx], sign)
 
 
+@pytest.mark.parametrize("logs,batch", [("12,8", 17), ("8,12", 17), ("12,10", 5), ("12,12", 1)])
+def test_cluster_pass(logs, batch, monkeypatch):
+    """The 4096-long pass on a cluster of four CTAs (cpass.cu: rows = q mod 4 per CTA, 1024-point
+    sub-DFTs, peer-shared bulk-copy exchange, radix-4 combine), first and later positions; the
+    persistent clusters run several tiles each (mbarrier phases flip), sampled vs the oracle."""
+    monkeypatch.setenv("FFTC_PASS_LOGS", logs)
+    monkeypatch.setenv("FFTC_PASS", "cp4096_q4_r32x32_c8b2")
+    n = sum(int(e) for e in logs.split(","))
+    N = 1 << n
+    x = synth.uniform_c64(N, batch, seed=n + 13)
+    with fftc.Plan(N, batch, -1) as p:
+        assert "cp4096_q4_r32x32_c8b2" in p.describe(), p.describe()
+    idx = sample_idx(batch, n_rand=3)
+    for sign in (-1, 1):
+        check(gpu_fft(x, sign)[idx], x[idx], sign)
+
+
 # ---------------------------------------------------------------- the paper's own check (P:217)
 def test_paper_protocol_p217_on_gpu():
     """The paper's accuracy experiment on the GPU path: random inputs, N = 32..1024,
