@@ -135,7 +135,7 @@ __global__ void __cluster_dims__(kQ, 1, 1) __launch_bounds__(P::THREADS, 1)
         mbar_arrive_remote(dsmem_map(smem_u32(&ack), (q + j) % kQ));
       });
       // every peer consumed this CTA's chunks: the tile buffer is free, the peers' slots too
-      mbar_wait_cluster(&ack, it & 1);
+      mbar_wait(&ack, it & 1);
       if (tile_of(it + kNBuf) < T) {
         fence_proxy_async_smem();
         issue(tile_of(it + kNBuf), k);

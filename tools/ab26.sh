@@ -1,6 +1,6 @@
 # cluster 4096-long pass candidates: parity against numpy (fp64) and timing against the default plans
 OUT=gpurun_out/ab26; mkdir -p $OUT
-for PASSN in cp4096_q4_r32x32_c8b2 cp4096_q4_r16x16x4_c8t64; do
+for PASSN in cp4096_q4_r32x32_c8b2; do
 FFTC_PASS=$PASSN python - >> $OUT/par.txt 2>&1 <<'PY'
 import os, sys, numpy as np, torch
 sys.path.insert(0, '.')
@@ -19,7 +19,7 @@ PY
 done
 for i in 1 2; do
 TAG=default python tools/time_sizes.py 16777216 4194304 >> $OUT/t.jsonl 2>&1
-for PASSN in cp4096_q4_r32x32_c8b2 cp4096_q4_r16x16x4_c8t64; do
+for PASSN in cp4096_q4_r32x32_c8b2; do
 FFTC_PASS=$PASSN FFTC_PASS_LOGS=12,12 TAG=$PASSN python tools/time_sizes.py 16777216 >> $OUT/t.jsonl 2>&1
 FFTC_PASS=$PASSN FFTC_PASS_LOGS=12,10 TAG=$PASSN python tools/time_sizes.py 4194304 >> $OUT/t.jsonl 2>&1
 done
