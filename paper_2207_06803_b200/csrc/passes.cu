@@ -203,6 +203,8 @@ static const PassEntry kPasses[] = {
     FFTC_PASS4("p4096_r16x16x16_c4b1", 4096, PRad_16x16x16, 128, 1, 1, 16, 16, 16),
     // a cluster of 4 CTAs per 8-column tile, each the 1024-point sub-DFT of one row residue class
     {4096, 2, {32, 32}, 32, 8, &launch_cpass4096, "cp4096_q4_r32x32_c8b2", 4},
+    // the tile being computed in registers, 4 columns, next tile's TMA load in shared memory
+    {4096, 3, {16, 16, 16}, 128, 4, &launch_rpass4096, "rp4096_r16x16x16_c4"},
 };
 
 // the entry of length L among a comma-separated list of candidate names
@@ -233,7 +235,7 @@ const PassEntry* find_pass(int L, long long N, bool first) {
   // 1.58 ms); first passes of length <= 512 keep two buffers (no TMA store to wait for)
   const char* pick = nullptr;
   if (L == 1024) pick = "p1024_r32x32_c8b3";
-  else if (L == 4096) pick = "p4096_r16x16x16_c2b3";
+  else if (L == 4096) pick = "rp4096_r16x16x16_c4";  // profiles/r02g: 2^22 1.90 -> 1.78, 2^23 2.11 -> 1.93 ms
   else if (L == 2048) pick = first ? "p2048_r16x16x8_c2b3" : "p2048_r16x16x8_c4b3";
   else if (L == 512 && !first) pick = "p512_r16x32_c8t32b3";
   else if (L == 256 && !first && N > (1LL << 20)) pick = "p256_r16x16_b3m2";
@@ -352,9 +354,11 @@ int pass_split(long long N, int* Ls, int max) {
   if (n >= 21 && n <= 23 && maxlog >= 10 && max >= 2) {
     // two passes with 2048/4096-long passes (2-column tiles first, 4-column tiles -- full 32-byte
     // sectors per strided row -- later): 2^21 [2048, 1024] 2.26 -> 1.69 ms, 2^22 [2048, 2048]
-    // 2.20 -> 1.89 ms, 2^23 [4096, 2048] 2.22 -> 2.13 ms (profiles/r01j/long_first_pass.jsonl)
-    Ls[0] = n == 21 ? 2048 : n == 22 ? 2048 : 4096;
-    Ls[1] = n == 21 ? 1024 : 2048;
+    // 2.20 -> 1.89 ms, 2^23 [4096, 2048] 2.22 -> 2.13 ms (profiles/r01j/long_first_pass.jsonl);
+    // round 2, the register-resident 4096-long first pass (rpass.cu): 2^22 [4096, 1024] 1.78 ms,
+    // 2^23 [4096, 2048] 1.93 ms (profiles/r02g)
+    Ls[0] = n == 21 ? 2048 : 4096;
+    Ls[1] = n == 21 ? 1024 : n == 22 ? 1024 : 2048;
     return 2;
   }
   int p = (n + 7) / 8;

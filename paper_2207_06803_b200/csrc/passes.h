@@ -37,6 +37,11 @@ cudaError_t launch_cpass4096(bool first, const CUtensorMap& tin, const CUtensorM
                              const float2* tw, const float2* twA, const float2* twB, const PassGeom& g, int conj_in,
                              int conj_out, cudaStream_t st);
 
+// 4096-long pass with the tile being computed held in registers (rpass.cu): 4-column tiles, the
+// next tile's TMA load and a half-tile exchange buffer in shared memory, outputs stored by the threads
+cudaError_t launch_rpass4096(bool first, const CUtensorMap& tin, const CUtensorMap& tout, float2* out,
+                             const float2* tw, const float2* twA, const float2* twB, const PassGeom& g, int conj_in,
+                             int conj_out, cudaStream_t st);
 constexpr int kMaxPasses = 6;
 struct PassPlanData {
   long long N = 0;

@@ -93,7 +93,7 @@ def test_planner_passes():
         # 2^17..2^20: two passes of <= 1024, 2^21..2^23: two passes with 2048/4096-long ones,
         # 2^25..2^28: three (last 256); else ceil(n/8) of <= 256
         if n in (21, 22, 23):
-            assert Ls == {21: [2048, 1024], 22: [2048, 2048], 23: [4096, 2048]}[n], (n, Ls)
+            assert Ls == {21: [2048, 1024], 22: [4096, 1024], 23: [4096, 2048]}[n], (n, Ls)
             continue
         big = 17 <= n <= 20 or 25 <= n <= 28
         want = 2 if 17 <= n <= 20 else 3 if 25 <= n <= 28 else (n + 7) // 8

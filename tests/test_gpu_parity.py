@@ -170,6 +170,25 @@ def test_cluster_pass(logs, batch, monkeypatch):
         check(gpu_fft(x, sign)[idx], x[idx], sign)
 
 
+@pytest.mark.parametrize("logs,batch", [("12,8", 17), ("8,12", 17), ("12,10", 5), ("11,12", 3), ("12,12", 1),
+                                        ("12,12", 2)])
+def test_register_pass(logs, batch, monkeypatch):
+    """The 4096-long pass with its tile held in registers (rpass.cu: 4-column tiles, two-half
+    stage exchanges, outputs stored from registers), first and later positions, persistent CTAs
+    running many tiles (the mbarrier phase flips), sampled vs the oracle, both signs."""
+    monkeypatch.setenv("FFTC_PASS_LOGS", logs)
+    name = "rp4096_r16x16x16_c4"
+    monkeypatch.setenv("FFTC_PASS", name)
+    n = sum(int(e) for e in logs.split(","))
+    N = 1 << n
+    x = synth.uniform_c64(N, batch, seed=n + 17)
+    with fftc.Plan(N, batch, -1) as p:
+        assert name + " " in p.describe() or name + "," in p.describe(), p.describe()
+    idx = sample_idx(batch, n_rand=3)
+    for sign in (-1, 1):
+        check(gpu_fft(x, sign)[idx], x[idx], sign)
+
+
 # ---------------------------------------------------------------- the paper's own check (P:217)
 def test_paper_protocol_p217_on_gpu():
     """The paper's accuracy experiment on the GPU path: random inputs, N = 32..1024,
