@@ -4,7 +4,8 @@
 
 Each variant's plan is made with its environment (FFTC_PASS, FFTC_PASS_LOGS, ...), checked once
 against numpy's fp64 FFT on two transforms (rel L2), then all variants are timed in alternating
-rounds (CUDA events, batch = 2^28 / N, median ms per 2^28 elements).  JSON line per variant."""
+rounds (CUDA events, batch = 2^26 / N up to 4096 else 2^28 / N, median ms; frac_copy_peak = one
+HBM round trip (16 B per element) against the measured 6557 GB/s).  JSON line per variant."""
 import json
 import os
 import sys
@@ -36,7 +37,7 @@ def main():
         label, _, rest = a.partition(":")
         env = dict(kv.split("=", 1) for kv in rest.split(";") if kv)
         variants.append((label, env))
-    batch = max(1, (1 << 28) // N)
+    batch = max(1, ((1 << 26) if N <= 4096 else (1 << 28)) // N)  # the BASELINE configs' sizes
     g = torch.Generator(device="cuda").manual_seed(0)
     x = torch.randn(batch, N, dtype=torch.complex64, device="cuda", generator=g)
     y = torch.empty_like(x)
@@ -77,6 +78,7 @@ def main():
         rec["ms_median"] = round(ts[len(ts) // 2], 4)
         rec["ms_min"] = round(ts[0], 4)
         rec["ms_per_2^28"] = round(rec["ms_median"] * (1 << 28) / (N * batch), 4)
+        rec["frac_copy_peak"] = round(16.0 * N * batch / (rec["ms_median"] * 1e-3) / 6556.8e9, 4)
         print(json.dumps(rec), flush=True)
         p.close()
 
