@@ -97,6 +97,8 @@ cudaError_t exec_local(const fftc_plan* p, const float2* in, float2* out, long l
       return jit_launch(p->jk, in, out, p->d_tw, batch, conj, st);
     case KIND_DIRECT:
       return direct_execute(p->N, in, out, p->d_direct, batch, st);
+    case KIND_CLUSTER:
+      return c16_execute(in, out, batch, conj, p->d_tw, p->d_twA, p->d_twB, st);
     case KIND_FOURSTEP: {
       const ColGeom g = fourstep_cols_geom(p->ce, p->N, p->K);
       cudaError_t e = p->ce->launch(in, work, p->d_tw, p->d_twA, p->d_twB, g, batch, conj, 0, st);
@@ -349,6 +351,16 @@ fftc_plan* fftc_plan_create(int64_t N, int64_t batch, int sign) {
       return p;
     }
   }
+  // N = 65536 in one HBM round trip on a cluster of eight CTAs (c16.cu; FFTC_LARGE=cluster)
+  if (N == 65536 && large && strcmp(large, "cluster") == 0 && c16_available()) {
+    p->kind = KIND_CLUSTER;
+    const int R16[2] = {16, 16};
+    p->d_tw = upload_stage_table(256, R16, 2, &err);
+    if (err == cudaSuccess) p->d_twA = upload_root_table(65536, 256, 1, &err);
+    if (err == cudaSuccess) p->d_twB = upload_root_table(65536, 257, 256, &err);
+    if (err != cudaSuccess) return fail(p, from_cuda(err));
+    return p;
+  }
   // multi-pass TMA path for powers of two (FFTC_LARGE=fourstep selects the two-pass kernels)
   int Ls[kMaxPasses];
   const int np = pass_split(N, Ls, kMaxPasses);
@@ -535,6 +547,7 @@ int fftc_plan_launches(const fftc_plan* p) {
     case KIND_GPASS: return p->batch > 0 ? p->gp.p : 0;
     case KIND_JIT: return p->batch > 0 ? 1 : 0;
     case KIND_DIRECT: return p->batch > 0 ? 1 : 0;
+    case KIND_CLUSTER: return p->batch > 0 ? 1 : 0;
     case KIND_DIST: return dist_launches(p->dist);
   }
   return -1;
@@ -575,6 +588,12 @@ int fftc_plan_describe(const fftc_plan* p, char* buf, size_t len) {
       break;
     case KIND_DIST:
       n += dist_describe(p->dist, tmp + n, sizeof(tmp) - n);
+      break;
+    case KIND_CLUSTER:
+      n += snprintf(tmp + n, sizeof(tmp) - n,
+                    "kind=cluster N=%lld batch=%lld sign=%d split=256x256 kernel=k_c16(cluster of 8 CTAs, DSMEM row "
+                    "exchange, one HBM round trip) launches=1",
+                    (long long)p->N, (long long)p->batch, p->sign);
       break;
     case KIND_DIRECT:
       n += snprintf(tmp + n, sizeof(tmp) - n,

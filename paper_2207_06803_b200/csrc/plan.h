@@ -6,6 +6,7 @@
 #include "fourstep.h"
 #include "gpass.h"
 #include "jit.h"
+#include "c16.h"
 #include "direct_tc.h"
 #include "l2pass.h"
 #include "passes.h"
@@ -13,7 +14,8 @@
 
 namespace fftc {
 
-enum PlanKind : int { KIND_COPY = 0, KIND_FUSED = 1, KIND_GENERIC = 2, KIND_FOURSTEP = 3, KIND_DIST = 4, KIND_PASSES = 5, KIND_L2 = 6, KIND_GPASS = 7, KIND_JIT = 8, KIND_DIRECT = 9 };
+enum PlanKind : int { KIND_COPY = 0, KIND_FUSED = 1, KIND_GENERIC = 2, KIND_FOURSTEP = 3, KIND_DIST = 4, KIND_PASSES = 5, KIND_L2 = 6, KIND_GPASS = 7, KIND_JIT = 8, KIND_DIRECT = 9,
+                     KIND_CLUSTER = 10 };
 
 struct DistState;  // dist.cu
 

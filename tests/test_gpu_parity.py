@@ -189,6 +189,22 @@ def test_register_pass(logs, batch, monkeypatch):
         check(gpu_fft(x, sign)[idx], x[idx], sign)
 
 
+@pytest.mark.parametrize("batch", [1, 3, 17, 40])
+def test_cluster_single_pass_65536(batch, monkeypatch):
+    """N = 65536 in one HBM round trip on a cluster of eight CTAs (c16.cu: column DFT_256 per CTA,
+    rows delivered to their owner CTA through distributed shared memory, row DFT_256 with the
+    folded w_N^{rj}); batches above the number of resident clusters make every cluster run
+    several transforms (mbarrier phases and cluster-barrier rounds wrap), both signs."""
+    monkeypatch.setenv("FFTC_LARGE", "cluster")
+    N = 1 << 16
+    x = synth.normal_c64(N, batch, seed=batch + 29)
+    with fftc.Plan(N, batch, -1) as p:
+        assert "kind=cluster" in p.describe(), p.describe()
+    idx = sample_idx(batch, n_rand=4)
+    for sign in (-1, 1):
+        check(gpu_fft(x, sign)[idx], x[idx], sign)
+
+
 # ---------------------------------------------------------------- the paper's own check (P:217)
 def test_paper_protocol_p217_on_gpu():
     """The paper's accuracy experiment on the GPU path: random inputs, N = 32..1024,
