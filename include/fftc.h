@@ -110,12 +110,17 @@ int fftc_candidates(int64_t N, const char** names, int max);
 /* Two-level split for N: returns 1 (single pass: *M = N, *K = 1),
  * 2 (four-step: N = M*K, column DFT_M then row DFT_K), or -1 unsupported.
  * Powers of two above 4096 run the multi-pass path instead (fftc_plan_passes)
- * unless FFTC_LARGE=fourstep is set.                                       */
+ * unless the environment variable FFTC_LARGE selects another large-N path at
+ * plan creation: fourstep (the classic two-kernel four-step), l2 (all passes
+ * in one L2-resident kernel, 2^13..2^21), gpass (runtime-schedule passes) or
+ * cluster (N = 65536 only: one HBM round trip on a cluster of eight CTAs).  */
 int fftc_plan_split(int64_t N, int64_t* M, int64_t* K);
 
-/* Multi-pass split (host only): power-of-two N in [2^9, 2^48] as
- * p = ceil(log2 N / 8) passes of lengths L_s in [16, 256], product N,
- * each one level of Eq. 2 in Stockham form over HBM.  Writes up to `max`
+/* Multi-pass split (host only): power-of-two N in [2^9, 2^48] as p passes
+ * of lengths L_s (product N), each one level of Eq. 2 in Stockham form over
+ * HBM: 2^17..2^20 two passes of <= 1024, 2^21..2^23 two passes with a
+ * 2048/4096-long first pass, 2^25..2^28 three passes ending in 256, every
+ * other N ceil(log2 N / 8) passes of lengths in [16, 256].  Writes up to `max`
  * lengths, returns p, or -1 if N is not such a power of two.              */
 int fftc_plan_passes(int64_t N, int* lengths, int max);
 
