@@ -27,17 +27,19 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 PEAK, NOMINAL = 6556.8, 8000.0
 
 
-def ncu_fill(rows, workload):
-    """Add the committed per-job ncu numbers (profiles/ncu_jobs_<w>.json) to rows that lack them."""
+def ncu_fill(rows, workload, peak=None):
+    """Set the committed per-job ncu numbers (profiles/ncu_jobs_<w>.json, the latest per-job launch
+    lists) on every row, as a percentage of the line's own measured peak (PEAK if not given)."""
+    peak = peak or PEAK
     p = os.path.join(ROOT, "profiles", "ncu_jobs_%s.json" % workload)
     if not os.path.exists(p):
         return
     m = {(j["N"], j["sign"]): j for j in json.load(open(p))["jobs"]}
     for r in rows:
         j = m.get((r["N"], r["sign"]))
-        if j and "ncu_dram_GBs" not in r:
+        if j:
             r.update({"ncu_us": j["us"], "ncu_dram_GBs": j["dram_GBs"], "ncu_dram_bytes_per_elt": j["dram_bytes_per_elt"],
-                      "pct_peak_measured": round(100 * j["dram_GBs"] / PEAK, 1),
+                      "pct_peak_measured": round(100 * j["dram_GBs"] / peak, 1),
                       "pct_peak_nominal": round(100 * j["dram_GBs"] / NOMINAL, 1)})
 
 
@@ -65,9 +67,9 @@ def render(lines, sources):
         out += ["End to end through `fftc_execute_host` (pinned host buffers, PCIe): %s GFLOP/s. Oracle (fp64 O2, "
                 "%s cores, %s): %s GFLOP/s on a bounded sample (reported baseline only)." %
                 (fmt(e.get("value")), cb.get("cores"), cb.get("cpu_model"), fmt(cb.get("value"), 2)), ""]
-        ncu_fill(d["per_job"], "c2")
-        out += ["| N | sign | batch | µs (mean / median / p90) | GFLOP/s | eff. GB/s | ncu µs | ncu DRAM GB/s | % of 6557 | "
-                "% of 8000 | plan |", "|---|---|---|---|---|---|---|---|---|---|---|"]
+        ncu_fill(d["per_job"], "c2", rl["peak"])
+        out += ["| N | sign | batch | µs (mean / median / p90) | GFLOP/s | eff. GB/s | ncu µs | ncu DRAM GB/s | %% of %.0f | "
+                "%% of 8000 | plan |" % rl["peak"], "|---|---|---|---|---|---|---|---|---|---|---|"]
         for j in d["per_job"]:
             kern = re.search(r"kernel=(\S+)", j["plan"])
             out.append("| %d | %+d | %d | %.1f / %.1f / %.1f | %.0f | %.0f | %s | %s | %s | %s | %s |" % (
@@ -79,7 +81,7 @@ def render(lines, sources):
             r = d.get(w)
             if not r or "jobs" not in r:
                 continue
-            ncu_fill(r["jobs"], w)
+            ncu_fill(r["jobs"], w, rl["peak"])
             out += ["**%s** — %.0f GFLOP/s; fraction of the §8(d) bound (%d B per element): min %.3f." %
                     (title, r["value"], bpe, r["frac_min"]), "",
                     "| N | sign | µs | GFLOP/s | HBM passes | frac (§8(d) bound) | ncu DRAM GB/s | ncu B/element |",
