@@ -24,6 +24,7 @@
 // early.  Measured on B200 (profiles/r02g): the same staged through shared memory and sent as
 // eight 8 KB bulk copies ran at the same speed.
 #include <cuda.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "c16.h"
@@ -35,9 +36,8 @@ namespace fftc {
 
 namespace {
 
-constexpr int kN = 65536, kS = 256, kR = 16, kQ = 8, kCols = kS / kQ, kThreads = 512;
-constexpr uint32_t kTileBytes = (uint32_t)kS * kCols * 8u;  // 64 KB per CTA per transform
-constexpr int kCPitch = 257;                                 // C rows in the row phase (odd pitch)
+constexpr int kN = 65536, kS = 256, kR = 16;
+constexpr int kCPitch = 257;  // B rows in the row phase (odd pitch)
 
 __device__ __forceinline__ void cl_wait_acquire() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
 __device__ __forceinline__ void cl_arrive_relaxed() {
@@ -87,13 +87,20 @@ __device__ __forceinline__ void stage_tw(const float2* __restrict__ tw, int m, f
 // Cluster barrier (relaxed, one arrive and one wait per iteration): the wait before delivering
 // transform t into B[t & 1] pairs with the arrive after the peers consumed B[t & 1] (transform
 // t - 2), which every CTA makes after its row-phase reads of t - 1 ... of the buffer it frees.
-__global__ void __cluster_dims__(kQ, 1, 1) __launch_bounds__(kThreads, 1)
+// Q CTAs per cluster (launched with a runtime cluster dimension): CTA p owns kCols = 256 / Q
+// columns in the column phase and as many rows in the row phase, with 16 kCols threads (one
+// radix-16 butterfly each per stage).  Q = 8: 64 KB per CTA and transform, one CTA per SM (512
+// threads, 194 KB of shared memory); Q = 16: 32 KB, 256 threads, two CTAs per SM.
+template <int Q>
+__global__ void __launch_bounds__(16 * (kS / Q), Q / 8)
     k_c16(const __grid_constant__ CUtensorMap tin, float2* __restrict__ out, const float2* __restrict__ tw,
           const float2* __restrict__ twA, const float2* __restrict__ twB, long long batch, float csign_in,
           float csign_out) {
+  constexpr int kQ = Q, kCols = kS / Q;
+  constexpr uint32_t kTileBytes = (uint32_t)kS * kCols * 8u;  // per CTA and transform
   extern __shared__ unsigned char smraw[];
   float2* A = reinterpret_cast<float2*>(smraw + ((128u - (smem_u32(smraw) & 127u)) & 127u));
-  float2* Bbuf = A + kS * kCols;  // two [32][kCPitch] buffers
+  float2* Bbuf = A + kS * kCols;  // two [kCols][kCPitch] buffers
   __shared__ __align__(8) uint64_t full, bfull[2];
   const int p = (int)cluster_ctarank();
   const long long cid = blockIdx.x / kQ, ncl = gridDim.x / kQ;
@@ -204,14 +211,15 @@ __global__ void __cluster_dims__(kQ, 1, 1) __launch_bounds__(kThreads, 1)
       });
       Codelet<kR>::run(v);
     }
-    // ---- deliver Y[j][32 p + rl] to CTA j div 32 (= s / 2), row j mod 32, buffer it & 1
+    // ---- deliver Y[j][kCols p + rl] (j = ja + 16 s) to CTA j div kCols = 16 s div kCols, row
+    // j mod kCols = 16 s mod kCols + ja, buffer it & 1
     cl_wait_acquire();  // every CTA has consumed B[it & 1] (transform it - 2)
     const uint32_t boff = (uint32_t)((it & 1) * (kCols * kCPitch) + p * kCols + rl) * 8u;
     sfor<kR>([&](auto s_) {
       constexpr int s = decltype(s_)::value;
-      const int row = ja + 16 * (s & 1);
-      st_async_f2(dsmem_map(B_local + boff + (uint32_t)(row * kCPitch * 8), s / 2), v[s],
-                  dsmem_map(bfull_local + (uint32_t)((it & 1) * 8), s / 2));
+      constexpr int dst = 16 * s / kCols, row0 = 16 * s % kCols;
+      st_async_f2(dsmem_map(B_local + boff + (uint32_t)((row0 + ja) * kCPitch * 8), dst), v[s],
+                  dsmem_map(bfull_local + (uint32_t)((it & 1) * 8), dst));
     });
     // ---- row phase of the previous transform (its rows arrived during this column phase)
     if (it > 0) row_phase(it - 1, false);
@@ -240,50 +248,66 @@ encode_fn get_encode() {
 
 bool c16_available() { return get_encode() != nullptr; }
 
-cudaError_t c16_execute(const float2* in, float2* out, long long batch, int conj, const float2* tw256,
-                        const float2* twA, const float2* twB, cudaStream_t st) {
-  if (batch <= 0) return cudaSuccess;
-  encode_fn enc = get_encode();
-  if (!enc) return cudaErrorNotSupported;
-  // in as [batch][256 rows q][256 columns r], box [32 columns][256 rows][1]
-  CUtensorMap tin;
-  cuuint64_t dims[3] = {(cuuint64_t)kS, (cuuint64_t)kS, (cuuint64_t)batch};
-  cuuint64_t strides[2] = {(cuuint64_t)kS * 8, (cuuint64_t)kN * 8};
-  cuuint32_t box[3] = {(cuuint32_t)kCols, (cuuint32_t)kS, 1};
-  cuuint32_t es[3] = {1, 1, 1};
-  if (enc(&tin, CU_TENSOR_MAP_DATA_TYPE_INT64, 3, const_cast<float2*>(in), dims, strides, box, es,
-          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-    return cudaErrorInvalidValue;
+template <int Q>
+cudaError_t c16_launch(const CUtensorMap& tin, float2* out, long long batch, int conj, const float2* tw256,
+                       const float2* twA, const float2* twB, cudaStream_t st) {
+  constexpr int kCols = kS / Q, kThreads = 16 * kCols;
   constexpr size_t smem = (size_t)(kS * kCols + 2 * kCols * kCPitch) * sizeof(float2) + 128;
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = Q;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
   struct Setup {
     cudaError_t err;
     int clusters;
   };
   static PerDevice<Setup> setup_pd;
   const Setup& su = setup_pd.get([&] {
-    Setup s{cudaFuncSetAttribute(k_c16, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), 0};
-    if (s.err != cudaSuccess) return s;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(kQ, 1, 1);
-    cfg.blockDim = dim3(kThreads, 1, 1);
-    cfg.dynamicSmemBytes = smem;
-    cudaLaunchAttribute attr;
-    attr.id = cudaLaunchAttributeClusterDimension;
-    attr.val.clusterDim.x = kQ;
-    attr.val.clusterDim.y = 1;
-    attr.val.clusterDim.z = 1;
-    cfg.attrs = &attr;
-    cfg.numAttrs = 1;
-    if (s.err == cudaSuccess) s.err = cudaOccupancyMaxActiveClusters(&s.clusters, k_c16, &cfg);
+    Setup s{cudaFuncSetAttribute(k_c16<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), 0};
+    if (s.err == cudaSuccess && Q > 8)
+      s.err = cudaFuncSetAttribute(k_c16<Q>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t c = cfg;
+    c.gridDim = dim3(Q, 1, 1);
+    if (s.err == cudaSuccess) s.err = cudaOccupancyMaxActiveClusters(&s.clusters, k_c16<Q>, &c);
     if (s.err == cudaSuccess && s.clusters <= 0) s.err = cudaErrorNotSupported;
     return s;
   });
   if (su.err != cudaSuccess) return su.err;
   const long long ncl = batch < su.clusters ? batch : su.clusters;
-  k_c16<<<(unsigned)(ncl * kQ), kThreads, smem, st>>>(tin, out, tw256, twA, twB, batch, conj ? -1.f : 1.f,
-                                                      conj ? -1.f : 1.f);
-  return cudaGetLastError();
+  cfg.gridDim = dim3((unsigned)(ncl * Q), 1, 1);
+  return cudaLaunchKernelEx(&cfg, k_c16<Q>, tin, out, tw256, twA, twB, batch, conj ? -1.f : 1.f,
+                            conj ? -1.f : 1.f);
+}
+
+cudaError_t c16_execute(const float2* in, float2* out, long long batch, int conj, const float2* tw256,
+                        const float2* twA, const float2* twB, cudaStream_t st) {
+  if (batch <= 0) return cudaSuccess;
+  encode_fn enc = get_encode();
+  if (!enc) return cudaErrorNotSupported;
+  // cluster size 8 (one CTA per SM); FFTC_C16_Q=16: clusters of 16 with two CTAs per SM (measured
+  // 1.82 vs 1.73-1.79 ms per 2^28 elements: only 14 clusters of 16 fit, 20 % warps active)
+  const char* qs = getenv("FFTC_C16_Q");
+  const int q = qs && atoi(qs) == 16 ? 16 : 8;
+  // in as [batch][256 rows q][256 columns r], box [256 / Q columns][256 rows][1]
+  CUtensorMap tin;
+  cuuint64_t dims[3] = {(cuuint64_t)kS, (cuuint64_t)kS, (cuuint64_t)batch};
+  cuuint64_t strides[2] = {(cuuint64_t)kS * 8, (cuuint64_t)kN * 8};
+  cuuint32_t box[3] = {(cuuint32_t)(kS / q), (cuuint32_t)kS, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  if (enc(&tin, CU_TENSOR_MAP_DATA_TYPE_INT64, 3, const_cast<float2*>(in), dims, strides, box, es,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  if (q == 16) return c16_launch<16>(tin, out, batch, conj, tw256, twA, twB, st);
+  return c16_launch<8>(tin, out, batch, conj, tw256, twA, twB, st);
 }
 
 }  // namespace fftc
+

@@ -189,13 +189,16 @@ def test_register_pass(logs, batch, monkeypatch):
         check(gpu_fft(x, sign)[idx], x[idx], sign)
 
 
+@pytest.mark.parametrize("q", ["8", "16"])
 @pytest.mark.parametrize("batch", [1, 3, 17, 40])
-def test_cluster_single_pass_65536(batch, monkeypatch):
+def test_cluster_single_pass_65536(batch, q, monkeypatch):
     """N = 65536 in one HBM round trip on a cluster of eight CTAs (c16.cu: column DFT_256 per CTA,
     rows delivered to their owner CTA through distributed shared memory, row DFT_256 with the
     folded w_N^{rj}); batches above the number of resident clusters make every cluster run
-    several transforms (mbarrier phases and cluster-barrier rounds wrap), both signs."""
+    several transforms (mbarrier phases and cluster-barrier rounds wrap), both signs; clusters of 8
+    (one CTA per SM) and of 16 (two CTAs per SM)."""
     monkeypatch.setenv("FFTC_LARGE", "cluster")
+    monkeypatch.setenv("FFTC_C16_Q", q)
     N = 1 << 16
     x = synth.normal_c64(N, batch, seed=batch + 29)
     with fftc.Plan(N, batch, -1) as p:
