@@ -99,6 +99,7 @@ cudaError_t exec_local(const fftc_plan* p, const float2* in, float2* out, long l
       return direct_execute(p->N, in, out, p->d_direct, batch, st);
     case KIND_CLUSTER:
       return c16_execute(in, out, batch, conj, p->d_tw, p->d_twA, p->d_twB, st);
+
     case KIND_FOURSTEP: {
       const ColGeom g = fourstep_cols_geom(p->ce, p->N, p->K);
       cudaError_t e = p->ce->launch(in, work, p->d_tw, p->d_twA, p->d_twB, g, batch, conj, 0, st);
