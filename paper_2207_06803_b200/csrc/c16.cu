@@ -20,8 +20,9 @@
 // 512 threads per CTA, one radix-16 butterfly each per stage.  Rows travel as st.async remote
 // stores counted on the receiver's mbarrier (complete_tx, 64 KB per transform), so no release
 // fence waits for the global stores (a release cluster barrier compiled to MEMBAR.ALL.GPU and a
-// first version stalled on it); a relaxed cluster barrier keeps rows from overwriting a buffer
-// early.  Measured on B200 (profiles/r02g): the same staged through shared memory and sent as
+// first version stalled on it).  A sender delivers into B[x] only after every receiver has
+// arrived (remotely, CTA-scope release) on the sender's bfree[x] mbarrier -- no cluster barrier in
+// the loop, whose acquire wait also invalidated L1 (CCTL.IVALL) and with it the twiddle tables.  Measured on B200 (profiles/r02g): the same staged through shared memory and sent as
 // eight 8 KB bulk copies ran at the same speed.
 #include <cuda.h>
 #include <stdlib.h>
@@ -39,10 +40,6 @@ namespace {
 constexpr int kN = 65536, kS = 256, kR = 16;
 constexpr int kCPitch = 257;  // B rows in the row phase (odd pitch)
 
-__device__ __forceinline__ void cl_wait_acquire() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
-__device__ __forceinline__ void cl_arrive_relaxed() {
-  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-}
 // asynchronous 8-byte store into another CTA's shared memory, counted on that CTA's mbarrier
 // (complete_tx): no release fence -- the receiver's mbarrier wait makes the data visible
 __device__ __forceinline__ void st_async_f2(uint32_t addr, float2 v, uint32_t bar) {
@@ -83,10 +80,9 @@ __device__ __forceinline__ void stage_tw(const float2* __restrict__ tw, int m, f
 // rows leave by st.async as soon as they are computed) and then the row phase of t - 1, whose
 // rows arrived during the column phase -- the DSMEM delivery overlaps arithmetic instead of
 // being waited for.  Shared memory: A (the TMA tile; the column-phase stage exchange in place),
-// B[2] (incoming rows of two transforms, [32 rows][257]; the row-phase exchange in place).
-// Cluster barrier (relaxed, one arrive and one wait per iteration): the wait before delivering
-// transform t into B[t & 1] pairs with the arrive after the peers consumed B[t & 1] (transform
-// t - 2), which every CTA makes after its row-phase reads of t - 1 ... of the buffer it frees.
+// B[2] (incoming rows of two transforms, [rows][257]; the row-phase exchange in place).  Flow
+// control per buffer x: bfull[x] (the receiver's 64 KB of rows, complete_tx) and bfree[x] (the
+// sender may deliver transform t into B[x] once all receivers arrived after consuming t - 2).
 // Q CTAs per cluster (launched with a runtime cluster dimension): CTA p owns kCols = 256 / Q
 // columns in the column phase and as many rows in the row phase, with 16 kCols threads (one
 // radix-16 butterfly each per stage).  Q = 8: 64 KB per CTA and transform, one CTA per SM (512
@@ -101,7 +97,7 @@ __global__ void __launch_bounds__(16 * (kS / Q), Q / 8)
   extern __shared__ unsigned char smraw[];
   float2* A = reinterpret_cast<float2*>(smraw + ((128u - (smem_u32(smraw) & 127u)) & 127u));
   float2* Bbuf = A + kS * kCols;  // two [kCols][kCPitch] buffers
-  __shared__ __align__(8) uint64_t full, bfull[2];
+  __shared__ __align__(8) uint64_t full, bfull[2], bfree[2];
   const int p = (int)cluster_ctarank();
   const long long cid = blockIdx.x / kQ, ncl = gridDim.x / kQ;
   const int t = (int)threadIdx.x;
@@ -113,14 +109,16 @@ __global__ void __launch_bounds__(16 * (kS / Q), Q / 8)
     mbar_init(&full, 1);
     mbar_init(&bfull[0], 1);
     mbar_init(&bfull[1], 1);
+    mbar_init(&bfree[0], kQ);  // one arrive from every receiver once it has consumed B[x]
+    mbar_init(&bfree[1], kQ);
     fence_mbarrier_init_cluster();
   }
   cluster_sync_all();  // every CTA's barriers exist before a peer signals them
   if (t == 0 && cid < batch) issue(cid);
-  const uint32_t B_local = smem_u32(Bbuf), bfull_local = smem_u32(&bfull[0]);
+  const uint32_t B_local = smem_u32(Bbuf), bfull_local = smem_u32(&bfull[0]), bfree_local = smem_u32(&bfree[0]);
   const long long nt = cid < batch ? (batch - 1 - cid) / ncl + 1 : 0;  // this cluster's transforms
-  // row phase of the cluster's transform `it` (rows in B[it & 1]); `last`: no later delivery
-  auto row_phase = [&](long long it, bool last) {
+  // row phase of the cluster's transform `it` (rows in B[it & 1])
+  auto row_phase = [&](long long it) {
     float2 v[kR];
     float2* B = Bbuf + (it & 1) * (kCols * kCPitch);
     const long long b = cid + it * ncl;
@@ -160,9 +158,13 @@ __global__ void __launch_bounds__(16 * (kS / Q), Q / 8)
         v[s] = cmul(v[s], w[s]);
       });
       // B[it & 1] consumed (every loaded value used above): expect transform it + 2's rows in it
-      if (t == 0 && it + 2 < nt) mbar_arrive_expect_tx(&bfull[it & 1], kTileBytes);
-      fence_proxy_async_smem();  // generic reads of B before the peers' asynchronous stores into it
-      if (!last) cl_arrive_relaxed();
+      if (it + 2 < nt) {  // B[it & 1] will receive transform it + 2
+        if (t == 0) mbar_arrive_expect_tx(&bfull[it & 1], kTileBytes);
+        fence_proxy_async_smem();  // generic reads of B before the peers' asynchronous stores into it
+        __syncthreads();           // every thread has consumed B[it & 1]
+        // tell every sender (release at CTA scope orders this CTA's reads before its stores)
+        if (t < kQ) mbar_arrive_remote(dsmem_map(bfree_local + (uint32_t)((it & 1) * 8), (uint32_t)t));
+      }
       Codelet<kR>::run(v);
       float2* o = out + b * kN + j + kS * i2;
       sfor<kR>([&](auto s_) {
@@ -175,7 +177,6 @@ __global__ void __launch_bounds__(16 * (kS / Q), Q / 8)
     if (nt > 0) mbar_arrive_expect_tx(&bfull[0], kTileBytes);
     if (nt > 1) mbar_arrive_expect_tx(&bfull[1], kTileBytes);
   }
-  cl_arrive_relaxed();  // B[0] free
   for (long long it = 0; it < nt; ++it) {
     const long long b = cid + it * ncl;
     float2 v[kR];
@@ -213,7 +214,8 @@ __global__ void __launch_bounds__(16 * (kS / Q), Q / 8)
     }
     // ---- deliver Y[j][kCols p + rl] (j = ja + 16 s) to CTA j div kCols = 16 s div kCols, row
     // j mod kCols = 16 s mod kCols + ja, buffer it & 1
-    cl_wait_acquire();  // every CTA has consumed B[it & 1] (transform it - 2)
+    // every CTA has consumed B[it & 1] (transform it - 2): the receivers' arrives on bfree
+    if (it >= 2) mbar_wait(&bfree[it & 1], (uint32_t)(((it >> 1) - 1) & 1));
     const uint32_t boff = (uint32_t)((it & 1) * (kCols * kCPitch) + p * kCols + rl) * 8u;
     sfor<kR>([&](auto s_) {
       constexpr int s = decltype(s_)::value;
@@ -222,11 +224,11 @@ __global__ void __launch_bounds__(16 * (kS / Q), Q / 8)
                   dsmem_map(bfull_local + (uint32_t)((it & 1) * 8), dst));
     });
     // ---- row phase of the previous transform (its rows arrived during this column phase)
-    if (it > 0) row_phase(it - 1, false);
-    else cl_arrive_relaxed();  // nothing consumed yet: keep one arrive per iteration
+    if (it > 0) row_phase(it - 1);
   }
-  if (nt > 0) row_phase(nt - 1, true);
-  cl_wait_acquire();  // matches the last arrive
+  if (nt > 0) row_phase(nt - 1);
+  // nothing reaches this CTA's shared memory any more: every delivery into it completed before its
+  // bfull waits, and the receivers' bfree arrives stop two transforms before the end
 }
 
 typedef CUresult (*encode_fn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
