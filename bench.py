@@ -429,7 +429,12 @@ def c5_child(args, world):
         return {"error": "six-step child job not finished after %d s" % args.c5_timeout}
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
     if r.returncode != 0 or not lines:
-        return {"error": "six-step child job rc=%d: %s" % (r.returncode, (r.stderr or r.stdout)[-400:])}
+        # the ranks' own error lines (torchrun's summary at the end of stderr names no cause)
+        out = (r.stderr or "") + (r.stdout or "")
+        cause = [ln.strip() for ln in out.splitlines()
+                 if any(w in ln for w in ("Error", "error:", "FFTC_", "NCCL WARN", "what():"))
+                 and "elastic" not in ln and "errors.html" not in ln]
+        return {"error": "six-step child job rc=%d: %s" % (r.returncode, " | ".join(cause[-4:]) or out[-400:])}
     d = json.loads(lines[-1])
     return {k: d[k] for k in ("value", "unit", "ms_per_step", "n_gpus", "variants", "a2a_reference", "config") if k in d}
 
