@@ -29,7 +29,11 @@ CASES = [
     (143, 37, {"FFTC_JIT_GENERIC": "1"}),
     (6561, 3, {}), (11 * 4096, 2, {}), (100000, 1, {}),          # generated passes (ragged columns)
     (6561, 3, {"FFTC_JIT_PASS_GENERIC": "1"}),
-    (1 << 16, 3, {}), (1 << 22, 1, {}), (1 << 24, 1, {}),       # TMA pass kernels
+    (1 << 16, 3, {}), (1 << 22, 1, {}), (1 << 24, 1, {}),       # TMA pass kernels (2^22: register 4096 pass)
+    (1 << 24, 1, {"FFTC_PASS_LOGS": "12,12", "FFTC_PASS": "rp4096_r16x16x16_c4"}),  # register pass, later position
+    (1 << 20, 1, {"FFTC_PASS_LOGS": "12,8", "FFTC_PASS": "cp4096_q4_r32x32_c8b2"}),  # 4-CTA cluster pass
+    (1 << 16, 3, {"FFTC_LARGE": "cluster"}),                     # 8-CTA cluster single pass
+    (1 << 16, 5, {"FFTC_LARGE": "cluster", "FFTC_C16_Q": "16"}),  # 16-CTA clusters, two CTAs per SM
 ]
 
 

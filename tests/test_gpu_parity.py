@@ -171,7 +171,7 @@ def test_cluster_pass(logs, batch, monkeypatch):
 
 
 @pytest.mark.parametrize("logs,batch", [("12,8", 17), ("8,12", 17), ("12,10", 5), ("11,12", 3), ("12,12", 1),
-                                        ("12,12", 2)])
+                                        ("12,12", 2), ("12,4", 1), ("4,12", 3)])
 def test_register_pass(logs, batch, monkeypatch):
     """The 4096-long pass with its tile held in registers (rpass.cu: 4-column tiles, two-half
     stage exchanges, outputs stored from registers), first and later positions, persistent CTAs
