@@ -54,6 +54,20 @@ def test_graph_capture_l2_resident(monkeypatch):
     test_graph_capture_replays_eager_result("l2", lambda: fftc.Plan(1 << 16, 37, -1), 1 << 16, 37)
 
 
+def test_graph_capture_cluster_single_pass(monkeypatch):
+    """The 8-CTA cluster single pass for 2^16 (cudaLaunchKernelEx with a cluster dimension, st.async
+    row delivery, mbarrier flow control) inside a captured graph."""
+    monkeypatch.setenv("FFTC_LARGE", "cluster")
+    test_graph_capture_replays_eager_result("cluster", lambda: fftc.Plan(1 << 16, 37, -1), 1 << 16, 37)
+
+
+def test_graph_capture_register_pass(monkeypatch):
+    """2^24 as two register-resident 4096-long passes inside a captured graph."""
+    monkeypatch.setenv("FFTC_PASS_LOGS", "12,12")
+    monkeypatch.setenv("FFTC_PASS", "rp4096_r16x16x16_c4")
+    test_graph_capture_replays_eager_result("rpass", lambda: fftc.Plan(1 << 24, 2, 1), 1 << 24, 2)
+
+
 def test_concurrent_plans_from_host_threads():
     """Plans of every kind created and executed concurrently from 6 host threads, each on its
     own stream (first-use kernel setup and the JIT cache are thread-safe); results equal the
