@@ -3,8 +3,9 @@
     python tools/bench_extra.py > gpurun_out/extra.jsonl
 
 Rows: the tensor-core direct DFT vs the Stockham kernel (N = 16, 32), JIT sizes, the
-runtime-schedule passes for non-power-of-two large N, the L2-resident variant, and the
-six-step in loopback mode (P virtual ranks on one GPU).  Effective GB/s counts 16 B per
+runtime-schedule passes for non-power-of-two large N, the L2-resident variant, the 8-CTA cluster
+single pass for 2^16, 2^24 as two register-resident 4096-long passes, 2^22 / 2^23 (register 4096
+first pass, the defaults), and the six-step in loopback mode (P virtual ranks on one GPU).  Effective GB/s counts 16 B per
 element (one read + one write); `hbm_passes` says how often the data crosses HBM.
 """
 import json
@@ -73,6 +74,19 @@ def main():
         row("l2_resident", N, b, p, timed(p, x, y, 5), 1)
         p.close()
     del os.environ["FFTC_LARGE"]
+    for tag, N, env, passes in (("cluster_single_pass", 1 << 16, {"FFTC_LARGE": "cluster"}, 1),
+                                ("register_4096_two_pass", 1 << 24,
+                                 {"FFTC_PASS_LOGS": "12,12", "FFTC_PASS": "rp4096_r16x16x16_c4"}, 2),
+                                ("default_2^22", 1 << 22, {}, 2), ("default_2^23", 1 << 23, {}, 2)):
+        b = (1 << 28) // N
+        os.environ.update(env)
+        try:
+            p = fftc.Plan(N, b, -1)
+        finally:
+            for k in env:
+                del os.environ[k]
+        row(tag, N, b, p, timed(p, x, y, 5), passes)
+        p.close()
     del x, y
     torch.cuda.empty_cache()
     N = 1 << 30
