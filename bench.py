@@ -783,7 +783,7 @@ def main():
                     help="one GPU: run the six-step for P virtual ranks (all-to-alls = device copies)")
     ap.add_argument("--c5-flags", type=int, default=0,
                     help="six-step options: 1 = transposed output (no all-to-all #3), 2 = fused peer-store exchanges")
-    ap.add_argument("--c5-timeout", type=int, default=300, help="time limit of the c5 sub-record's job (N > 1)")
+    ap.add_argument("--c5-timeout", type=int, default=150, help="time limit of the c5 sub-record's job (N > 1)")
     ap.add_argument("--c5-variants", default="", help="--workload c5: time these exchange modes, e.g. 0,2,3")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the c3/c4 (N = 1) or c5 (N > 1) sub-records")
